@@ -1,0 +1,473 @@
+/*
+ * gvom_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU oracle of G-VOM's per-scan voxel-map
+ * update (arXiv 2109.13176, section III, lines P:80-146).  It is
+ * used ONLY by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg.  The product path (paper_2109_13176_b200/, csrc/)
+ * never includes, links or calls it, and it shares no code, header, table or
+ * helper with the CUDA path.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
+ *        (no -march=native, no FMA contraction: every float32 step below is
+ *        one IEEE round-to-nearest operation, in the order written).
+ *
+ * Each function cites the passage it follows.  The readings of the paper
+ * (SURVEY.md 8(c) O0-O11 and the ambiguity ledger A1-A28) are listed in
+ * DESIGN.md "Readings".  Pins: tests/test_oracle_*.py.  Parity status:
+ *   O0-O8: pinned (closed forms, brute force, invariants, golden G1-G3).
+ *   O9   : pinned (closed-form planes, numpy lstsq brute force, G4).
+ *   O10  : pinned by special cases / scenario / monotonicity (G5); the cone
+ *          geometry itself is "parity unpinned" against the paper (the only
+ *          source is the fig:neg_obs_search prose).
+ *   Threshold values (T_lo, T_hi, tau, T_neg, N, K_neg): parity unpinned --
+ *          the paper gives no values.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_MISS_SAT (1u << 30) /* A11: empty-voxel N_m saturates at 2^30 */
+#define OR_GLIM 4194304.0f     /* A5: |g_i| < 2^22 voxels */
+
+/* ------------------------------------------------------------------------ */
+/* O0 -- integer thresholds            */
+/* ------------------------------------------------------------------------ */
+void or_thresholds(double res, double min_obstacle_height, double max_obstacle_height,
+                   double density_threshold, double neg_obs_threshold, int64_t out[4]) {
+  out[0] = llround(min_obstacle_height / res * 65536.0); /* T_lo */
+  out[1] = llround(max_obstacle_height / res * 65536.0); /* T_hi */
+  out[2] = llround(density_threshold * 65536.0);         /* tau  */
+  out[3] = llround(neg_obs_threshold / res * 65536.0);   /* T_neg */
+}
+
+/* ------------------------------------------------------------------------ */
+/* O1 -- origin snapping, "an integer multiple of the map resolution"       */
+/* with the map "centered on the vehicle".  Reading A3.       */
+/* ------------------------------------------------------------------------ */
+void or_snap_origin(int32_t nx, int32_t ny, int32_t nz, double res, double z_center_frac,
+                    const double p[3], int64_t o[3]) {
+  o[0] = (int64_t)floor(p[0] / res + 0.5) - (int64_t)(nx / 2);
+  o[1] = (int64_t)floor(p[1] / res + 0.5) - (int64_t)(ny / 2);
+  o[2] = (int64_t)floor(p[2] / res + 0.5) - (int64_t)floor((double)nz * z_center_frac);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2 -- per-sensor affine into the map frame in voxel units (P:105        */
+/* "the odometry data then is used to transform the pointcloud into the    */
+/* map frame"; reading A4): A = f32(R/res), b = f32(t/res - o).            */
+/* pose: 3x4 row-major [R | t], sensor -> world.                           */
+/* ------------------------------------------------------------------------ */
+void or_affine(const double pose[12], double res, const int64_t o[3], float A[9], float b[3]) {
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) A[3 * i + j] = (float)(pose[4 * i + j] / res);
+    b[i] = (float)(pose[4 * i + 3] / res - (double)o[i]);
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3 -- transform one point: g_i = ((A_i0 x + A_i1 y) + A_i2 z) + b_i,     */
+/* each op float32 round-to-nearest.  Validity (A5): finite input,  */
+/* not the (0,0,0) no-return, |g_i| < 2^22.  Returns 1 if valid.            */
+/* ------------------------------------------------------------------------ */
+int or_transform_point(const float A[9], const float b[3], float x, float y, float z, float g[3]) {
+  if (!isfinite(x) || !isfinite(y) || !isfinite(z)) return 0;
+  if (x == 0.0f && y == 0.0f && z == 0.0f) return 0;
+  int ok = 1;
+  for (int i = 0; i < 3; ++i) {
+    float t0 = A[3 * i + 0] * x;
+    float t1 = A[3 * i + 1] * y;
+    float t2 = A[3 * i + 2] * z;
+    float acc = t0 + t1;
+    acc = acc + t2;
+    acc = acc + b[i];
+    g[i] = acc;
+    if (!(fabsf(acc) < OR_GLIM)) ok = 0;
+  }
+  return ok;
+}
+
+static int or_in_grid(int64_t x, int64_t y, int64_t z, int32_t nx, int32_t ny, int32_t nz) {
+  return x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz;
+}
+
+/* linear index, reading A2: L = z + nz*(x + nx*y) */
+static int64_t or_lin(int64_t x, int64_t y, int64_t z, int32_t nx, int32_t nz) {
+  return z + (int64_t)nz * (x + (int64_t)nx * y);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O5 -- "the lidar rays are traced".  Reading A10: 3D DDA         */
+/* (Amanatides-Woo) with a stateless float32 key per axis,                  */
+/*   key_a(V) = f32( f32( f32(V_a + [step_a>0]) - s_a ) * inv_a ),          */
+/* remaining-step caps rem_a = |E_a - S_a| and ties to the lowest axis.    */
+/* Every traversed in-grid voxel except the endpoint voxel E is a "miss"   */
+/* ("passed though the voxel but did not end in it"; A8).  The walk   */
+/* stops at E or when it leaves the grid (A7).  visit(L) is called per miss.*/
+/* ------------------------------------------------------------------------ */
+typedef void (*or_visit_fn)(void* ctx, int64_t x, int64_t y, int64_t z);
+
+static int64_t or_walk(int32_t nx, int32_t ny, int32_t nz, const float s[3], const float g[3],
+                       or_visit_fn visit, void* ctx) {
+  int64_t S[3], E[3], V[3], rem[3];
+  int step[3];
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    S[a] = (int64_t)floorf(s[a]);
+    E[a] = (int64_t)floorf(g[a]);
+    float d = g[a] - s[a];
+    step[a] = (E[a] > S[a]) ? 1 : ((E[a] < S[a]) ? -1 : 0);
+    rem[a] = (E[a] > S[a]) ? (E[a] - S[a]) : (S[a] - E[a]);
+    inv[a] = (rem[a] > 0) ? (1.0f / d) : 0.0f;
+    V[a] = S[a];
+  }
+  int64_t count = 0;
+  while (or_in_grid(V[0], V[1], V[2], nx, ny, nz) && (rem[0] + rem[1] + rem[2]) > 0) {
+    if (visit) visit(ctx, V[0], V[1], V[2]);
+    ++count;
+    int best = -1;
+    float bkey = 0.0f;
+    for (int a = 0; a < 3; ++a) {
+      if (rem[a] <= 0) continue;
+      float edge = (float)(V[a] + (step[a] > 0 ? 1 : 0));
+      float diff = edge - s[a];
+      float key = diff * inv[a];
+      if (best < 0 || key < bkey) {
+        best = a;
+        bkey = key;
+      }
+    }
+    V[best] += step[best];
+    rem[best] -= 1;
+  }
+  return count;
+}
+
+typedef struct {
+  int32_t* out;
+  int64_t cap, n;
+} or_list_ctx;
+
+static void or_list_visit(void* c, int64_t x, int64_t y, int64_t z) {
+  or_list_ctx* l = (or_list_ctx*)c;
+  if (l->n < l->cap) {
+    l->out[3 * l->n + 0] = (int32_t)x;
+    l->out[3 * l->n + 1] = (int32_t)y;
+    l->out[3 * l->n + 2] = (int32_t)z;
+  }
+  l->n++;
+}
+
+/* Test hook: the miss voxels of one ray, in walk order.  Returns the count
+ * (which may exceed cap; only the first cap entries are written). */
+int64_t or_traverse(int32_t nx, int32_t ny, int32_t nz, const float s[3], const float g[3],
+                    int32_t* out_xyz, int64_t cap) {
+  or_list_ctx l = {out_xyz, cap, 0};
+  return or_walk(nx, ny, nz, s, g, or_list_visit, &l);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3-O5 over one scan into dense per-voxel grids ("two passes are   */
+/* then done over the pointcloud").  Accumulates (call once per sensor).   */
+/*   hits[v]++, min_dz[v] = min, m1[v] += dz, m2[v] += dz^2 (O4, A12, A13) */
+/*   misses[v]++ for every miss voxel (O5).                                  */
+/* stats: [0] valid points, [1] invalid points, [2] in-grid hits,          */
+/*        [3] miss increments.                                              */
+/* Returns -4 if the sensor voxel floor(b) is outside the grid (A9).       */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  uint32_t* misses;
+  int32_t nx, nz;
+} or_miss_ctx;
+
+static void or_miss_visit(void* c, int64_t x, int64_t y, int64_t z) {
+  or_miss_ctx* m = (or_miss_ctx*)c;
+  m->misses[or_lin(x, y, z, m->nx, m->nz)] += 1u;
+}
+
+int or_sensor_inside(int32_t nx, int32_t ny, int32_t nz, const float b[3]) {
+  return or_in_grid((int64_t)floorf(b[0]), (int64_t)floorf(b[1]), (int64_t)floorf(b[2]), nx, ny,
+                    nz);
+}
+
+int or_integrate(int32_t nx, int32_t ny, int32_t nz, const float A[9], const float b[3],
+                 const float* pts /* [n][4] */, int64_t n, uint32_t* hits, uint32_t* misses,
+                 uint32_t* min_dz, uint64_t* m1, uint64_t* m2, int64_t stats[4]) {
+  if (!or_sensor_inside(nx, ny, nz, b)) return -4;
+  or_miss_ctx mc = {misses, nx, nz};
+  for (int64_t i = 0; i < n; ++i) {
+    float g[3];
+    if (!or_transform_point(A, b, pts[4 * i + 0], pts[4 * i + 1], pts[4 * i + 2], g)) {
+      stats[1]++;
+      continue;
+    }
+    stats[0]++;
+    /* O4 -- bin ("number of returns within the voxel ... height of the
+     * lowest return"): v = floor(g), qz = floor(f32(g_z * 65536)). */
+    int64_t vx = (int64_t)floorf(g[0]), vy = (int64_t)floorf(g[1]), vz = (int64_t)floorf(g[2]);
+    if (or_in_grid(vx, vy, vz, nx, ny, nz)) {
+      float qf = g[2] * 65536.0f; /* exact: power-of-two scaling */
+      int64_t qz = (int64_t)floorf(qf);
+      uint32_t dz = (uint32_t)(qz - 65536 * vz);
+      int64_t L = or_lin(vx, vy, vz, nx, nz);
+      hits[L] += 1u;
+      if (dz < min_dz[L]) min_dz[L] = dz;
+      m1[L] += (uint64_t)dz;
+      m2[L] += (uint64_t)dz * (uint64_t)dz;
+      stats[2]++;
+    }
+    /* O5 -- ray from the sensor to this return (whether or not E is in grid) */
+    stats[3] += or_walk(nx, ny, nz, b, g, or_miss_visit, &mc);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O6 -- frame map: "If a voxel ... is occupied then the lookup     */
+/* table array contains that voxel's index in the data array.  If the      */
+/* voxel is not occupied then the value ... is -1 - N_m".                   */
+/* Occupied iff hits >= 1; index = rank in L order (A2).                    */
+/* Returns k = number of occupied voxels.                                   */
+/* ------------------------------------------------------------------------ */
+int64_t or_frame_map(int64_t V, const uint32_t* hits, const uint32_t* misses,
+                     const uint32_t* min_dz, const uint64_t* m1, const uint64_t* m2, int32_t* lut,
+                     uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_min, uint64_t* d_m1,
+                     uint64_t* d_m2) {
+  int64_t k = 0;
+  for (int64_t L = 0; L < V; ++L) {
+    if (hits[L] >= 1u) {
+      lut[L] = (int32_t)k;
+      d_hits[k] = hits[L];
+      d_misses[k] = misses[L];
+      d_min[k] = min_dz[L];
+      d_m1[k] = m1[L];
+      d_m2[k] = m2[L];
+      ++k;
+    } else {
+      uint32_t nm = misses[L] < OR_MISS_SAT ? misses[L] : OR_MISS_SAT;
+      lut[L] = -1 - (int32_t)nm;
+    }
+  }
+  return k;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O7 -- combine the buffer: "offsetting each of the map indices by */
+/* the offset between the buffer map and the combined map ... The combined */
+/* map uses the location of the most recent buffer map as it's origin ...  */
+/* hits and misses being added together and minimum return heights         */
+/* compared and the minimum taken".  Source voxels outside the new bounds  */
+/* are dropped (A16).  Outputs dense merged grids (zero/0xFFFFFFFF init by  */
+/* this function).                                                          */
+/*   luts[k], d_*[k]: slot k's LUT [V] and data SoA; origins[3k..3k+2].     */
+/* ------------------------------------------------------------------------ */
+void or_combine(int32_t nx, int32_t ny, int32_t nz, int32_t K, const int32_t* const* luts,
+                const uint32_t* const* d_hits, const uint32_t* const* d_misses,
+                const uint32_t* const* d_min, const uint64_t* const* d_m1,
+                const uint64_t* const* d_m2, const int64_t* origins, const int64_t o[3],
+                uint64_t* H, uint64_t* Mi, uint32_t* mn, uint64_t* M1, uint64_t* M2) {
+  int64_t V = (int64_t)nx * ny * nz;
+  for (int64_t L = 0; L < V; ++L) {
+    H[L] = 0;
+    Mi[L] = 0;
+    mn[L] = 0xFFFFFFFFu;
+    M1[L] = 0;
+    M2[L] = 0;
+  }
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x)
+      for (int64_t z = 0; z < nz; ++z) {
+        int64_t L = or_lin(x, y, z, nx, nz);
+        for (int32_t k = 0; k < K; ++k) {
+          int64_t ux = x + (o[0] - origins[3 * k + 0]);
+          int64_t uy = y + (o[1] - origins[3 * k + 1]);
+          int64_t uz = z + (o[2] - origins[3 * k + 2]);
+          if (!or_in_grid(ux, uy, uz, nx, ny, nz)) continue;
+          int32_t e = luts[k][or_lin(ux, uy, uz, nx, nz)];
+          if (e >= 0) {
+            H[L] += d_hits[k][e];
+            Mi[L] += d_misses[k][e];
+            if (d_min[k][e] < mn[L]) mn[L] = d_min[k][e];
+            M1[L] += d_m1[k][e];
+            M2[L] += d_m2[k][e];
+          } else {
+            Mi[L] += (uint64_t)(-1 - (int64_t)e);
+          }
+        }
+      }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O8 -- column reduce.  Height: "the height of the minimum height  */
+/* return of the minimum height voxel within each column".  Positive        */
+/* obstacles: voxels "between the minimum obstacle height and       */
+/* maximum obstacle height" above the surface; "weighted average density"   */
+/* (A19: SH/SW with w = hits+misses); hard iff density >= threshold (A20).  */
+/* qs: fixed-point surface q_s = 65536 z* + mn(z*) (int32), defined u8.     */
+/* ------------------------------------------------------------------------ */
+void or_columns(int32_t nx, int32_t ny, int32_t nz, double res, int64_t o_z, int64_t T_lo,
+                int64_t T_hi, int64_t tau, const uint64_t* H, const uint64_t* Mi,
+                const uint32_t* mn, float* height, float* density, uint8_t* hard, uint8_t* soft,
+                int32_t* qs, uint8_t* defined) {
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) {
+      int64_t c = x + (int64_t)nx * y;
+      int64_t zs = -1;
+      for (int64_t z = 0; z < nz; ++z)
+        if (H[or_lin(x, y, z, nx, nz)] >= 1) {
+          zs = z;
+          break;
+        }
+      hard[c] = 0;
+      soft[c] = 0;
+      if (zs < 0) {
+        height[c] = NAN;
+        density[c] = NAN;
+        qs[c] = 0;
+        defined[c] = 0;
+        continue;
+      }
+      int64_t q_s = 65536 * zs + (int64_t)mn[or_lin(x, y, zs, nx, nz)];
+      qs[c] = (int32_t)q_s;
+      defined[c] = 1;
+      height[c] = (float)(((double)(o_z * 65536 + q_s) * res) / 65536.0);
+      uint64_t SH = 0, SW = 0;
+      for (int64_t z = 0; z < nz; ++z) {
+        int64_t L = or_lin(x, y, z, nx, nz);
+        if (H[L] < 1) continue;
+        int64_t dq = (65536 * z + (int64_t)mn[L]) - q_s;
+        if (dq >= T_lo && dq <= T_hi) {
+          SH += H[L];
+          SW += H[L] + Mi[L];
+        }
+      }
+      if (SH == 0) {
+        density[c] = 0.0f;
+        continue;
+      }
+      density[c] = (float)((double)SH / (double)SW);
+      if ((uint64_t)65536 * SH >= (uint64_t)tau * SW)
+        hard[c] = 1;
+      else
+        soft[c] = 1;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O9 -- slope and roughness: "least squares fitting of a plane     */
+/* taking an NxN square of pixels around the pixel of interest.  The       */
+/* roughness of that pixel is the average squared error."  Reading A22:    */
+/* defined, in-map window cells; centre must be defined; n >= min_pts;     */
+/* exact int64 normal equations solved by Cramer's rule.                   */
+/* ------------------------------------------------------------------------ */
+static int64_t or_det3(int64_t a, int64_t b, int64_t c, int64_t d, int64_t e, int64_t f, int64_t g,
+                       int64_t h, int64_t i) {
+  return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+}
+
+void or_slope_roughness(int32_t nx, int32_t ny, double res, int32_t N, int32_t min_pts,
+                        const int32_t* qs, const uint8_t* defined, float* slope, float* rough) {
+  int32_t r = (N - 1) / 2;
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) {
+      int64_t c = x + (int64_t)nx * y;
+      slope[c] = NAN;
+      rough[c] = NAN;
+      if (!defined[c]) continue;
+      int64_t n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0, Sz = 0, Suz = 0, Svz = 0;
+      for (int32_t v = -r; v <= r; ++v)
+        for (int32_t u = -r; u <= r; ++u) {
+          int64_t xx = x + u, yy = y + v;
+          if (xx < 0 || xx >= nx || yy < 0 || yy >= ny) continue;
+          int64_t cc = xx + (int64_t)nx * yy;
+          if (!defined[cc]) continue;
+          int64_t z = (int64_t)qs[cc] - (int64_t)qs[c];
+          n += 1;
+          Su += u;
+          Sv += v;
+          Suu += (int64_t)u * u;
+          Svv += (int64_t)v * v;
+          Suv += (int64_t)u * v;
+          Sz += z;
+          Suz += u * z;
+          Svz += v * z;
+        }
+      if (n < min_pts) continue;
+      /* M [a b c]^T = rhs, M = [[Suu Suv Su][Suv Svv Sv][Su Sv n]], rhs = (Suz, Svz, Sz) */
+      int64_t det = or_det3(Suu, Suv, Su, Suv, Svv, Sv, Su, Sv, n);
+      if (det == 0) continue;
+      int64_t Da = or_det3(Suz, Suv, Su, Svz, Svv, Sv, Sz, Sv, n);
+      int64_t Db = or_det3(Suu, Suz, Su, Suv, Svz, Sv, Su, Sz, n);
+      int64_t Dc = or_det3(Suu, Suv, Suz, Suv, Svv, Svz, Su, Sv, Sz);
+      double a = (double)Da / ((double)det * 65536.0);
+      double b = (double)Db / ((double)det * 65536.0);
+      slope[c] = (float)atan(sqrt(a * a + b * b));
+      double acc = 0.0;
+      for (int32_t v = -r; v <= r; ++v)
+        for (int32_t u = -r; u <= r; ++u) {
+          int64_t xx = x + u, yy = y + v;
+          if (xx < 0 || xx >= nx || yy < 0 || yy >= ny) continue;
+          int64_t cc = xx + (int64_t)nx * yy;
+          if (!defined[cc]) continue;
+          int64_t z = (int64_t)qs[cc] - (int64_t)qs[c];
+          int64_t e = det * z - Da * u - Db * v - Dc;
+          double de = (double)e;
+          acc += de * de;
+        }
+      double sc = res / 65536.0;
+      rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O10 -- negative obstacles (fig:neg_obs_search P:142).     */
+/* "For each pixel in the undefined region we search in each direction in  */
+/* a cone shape until a defined surface has been found or until a maximum  */
+/* search distance is reached ... If the maximum difference between any of */
+/* these assumed height is larger than the negative obstacle threshold     */
+/* that pixel is defined as a negative obstacle."  Readings A24, A25:      */
+/* 4 axis cones over Chebyshev rings; all defined cells of a cone's first  */
+/* non-empty ring join F; neg = |F| >= 2 and max F - min F > T_neg.        */
+/* ------------------------------------------------------------------------ */
+void or_negative(int32_t nx, int32_t ny, int32_t K, int64_t T_neg, const int32_t* qs,
+                 const uint8_t* defined, uint8_t* neg) {
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) {
+      int64_t c = x + (int64_t)nx * y;
+      neg[c] = 0;
+      if (defined[c]) continue;
+      int64_t fmin = INT64_MAX, fmax = INT64_MIN, fcount = 0;
+      for (int cone = 0; cone < 4; ++cone) {
+        for (int32_t k = 1; k <= K; ++k) {
+          int found = 0;
+          for (int32_t t = -k; t <= k; ++t) {
+            int64_t xx, yy;
+            if (cone == 0) {
+              xx = x + k;
+              yy = y + t;
+            } else if (cone == 1) {
+              xx = x - k;
+              yy = y + t;
+            } else if (cone == 2) {
+              xx = x + t;
+              yy = y + k;
+            } else {
+              xx = x + t;
+              yy = y - k;
+            }
+            if (xx < 0 || xx >= nx || yy < 0 || yy >= ny) continue;
+            int64_t cc = xx + (int64_t)nx * yy;
+            if (!defined[cc]) continue;
+            found = 1;
+            int64_t q = qs[cc];
+            if (q < fmin) fmin = q;
+            if (q > fmax) fmax = q;
+            fcount++;
+          }
+          if (found) break;
+        }
+      }
+      neg[c] = (fcount >= 2 && (fmax - fmin) > T_neg) ? 1 : 0;
+    }
+}
