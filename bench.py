@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the G-VOM per-scan map update on B200 (driver contract).
+
+One STEP = one full map update through the C ABI, i.e. every SURVEY.md 8(a)
+row on one scan: gvom_shift + gvom_integrate_scan (transform, bin, ray cast,
+LUT/data, buffer push) + gvom_compute_maps (combine K=8 buffer maps, column
+reduce, slope/roughness, negative obstacles) + gvom_export_2d of all 7 layers.
+
+Workload (default): BASELINE.json configs[1] -- an OS1-64-like 131,072-point
+scan over rolling terrain with trees and bushes, 256x256x64 voxels at 0.25 m.
+Frames cycle over `--frames` independently drawn scans of the same scene.
+
+value  = lidar points integrated per second over whole steps (all ranks),
+         inputs resident in HBM, L2 flushed (256 MiB write) between steps,
+         device time from CUDA events on the library's stream.
+e2e    = same metric through the public API with pinned HOST buffers: H2D of
+         the scan and D2H of all 7 layers inside every timed step.
+roofline = the dominant kernel (ray cast): algorithmic bytes per launch
+         (16 N + 8 M + 8 H) / its mean event-timed launch
+         duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the oracle (oracle/, single-threaded C) on the same workload.
+
+--impl reference runs the oracle as the reference arm (CPU; rank 0 only).
+N > 1 (torchrun): every rank runs its own frame stream (independent maps, no
+data-path collective; weak scaling); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lidar points/s integrated and map updates/s (256×256×64), % HBM roofline"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="gvom", choices=["gvom", "reference"])
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
+    ap.add_argument("--frames", type=int, default=4, help="distinct scans cycled")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_workload(cfg_index: int, frames: int, rank: int):
+    from paper_2109_13176_b200 import synth
+    seed = 13176 + cfg_index + 1000 * rank
+    if cfg_index == 0:
+        return synth.config1(seed=seed)
+    if cfg_index == 1:
+        return synth.config2(seed=seed, n_frames=frames)
+    if cfg_index == 2:
+        return synth.config3(speed=12.0, n_frames=max(frames, 8), seed=seed)
+    if cfg_index == 3:
+        return synth.config4(seed=seed)
+    return synth.config5(seed=seed)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.f is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_run(w, budget_s: float, max_frames: int = 1000):
+    """The oracle as it stands on this host (single thread), bounded by budget."""
+    from oracle import oracle as O
+    om = O.OracleMap(w.grid)
+    t0 = time.perf_counter()
+    frames = pts = 0
+    while frames < max_frames:
+        f = w.frames[frames % len(w.frames)]
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in f.scans])
+        om.compute_maps()
+        frames += 1
+        pts += f.n_points
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    integ = om.times.get("integrate", 0.0) + om.times.get("frame_map", 0.0)
+    return dict(value=pts / dt, unit="points/s", cores=1, kind="oracle",
+                sample=f"{frames} full map updates ({pts} points) of {w.name}, "
+                       f"single-threaded C oracle, {dt:.1f} s",
+                updates_per_s=frames / dt, integrate_points_per_s=pts / integ if integ else None,
+                host_cpu=_cpu_model(), host_cores=os.cpu_count())
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    w = load_workload(args.config, args.frames, 0)
+    budget = float(os.environ.get("GVOM_REF_BUDGET_S", "60"))
+    # warmup: one untimed update; then timed updates bounded by the budget
+    from oracle import oracle as O
+    om = O.OracleMap(w.grid)
+    f = w.frames[0]
+    om.shift(f.vehicle_xyz)
+    om.integrate([(s.points, s.pose) for s in f.scans])
+    om.compute_maps()
+    r = oracle_run(w, budget, max_frames=max(1, args.steps))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 / r["updates_per_s"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
+        "config": {"workload": w.name, "points_per_scan": w.points_per_frame,
+                   "grid": f"{w.grid['nx']}x{w.grid['ny']}x{w.grid['nz']}@{w.grid['res']}m",
+                   "buffer_frames": w.grid["buffer_frames"]},
+        "map_updates_per_s": r["updates_per_s"],
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2109_13176_b200 import GvomMap
+    w = load_workload(args.config, args.frames, rank)
+    frames = w.frames
+    npts = w.points_per_frame
+    stream = torch.cuda.Stream(device=dev)
+    m = GvomMap(w.grid, max_points_per_frame=npts, device=dev, stream=stream)
+    dev_frames = [[(torch.from_numpy(s.points).to(dev), s.pose, s.rings) for s in f.scans]
+                  for f in frames]
+    out = {k: torch.empty((m.ny, m.nx), dtype=(torch.uint8 if k in ("hard", "soft", "neg")
+                                               else torch.float32), device=dev)
+           for k in ("height", "density", "hard", "soft", "neg", "slope", "roughness")}
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step(i, scans, outs):
+        f = frames[i % len(frames)]
+        m.shift(f.vehicle_xyz)
+        m.integrate_scan(scans)
+        m.compute_maps()
+        m.export_layers(outs)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i, dev_frames[i % len(frames)], out)
+        stream.synchronize()
+        # ---- timed region: device-resident inputs --------------------------
+        m.set_timing(True)
+        m.stage_times()  # clear
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        launches0 = m.launch_count()
+        barrier()
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()  # L2 flush, outside the step events
+                ev[i][0].record(stream)
+                step(i, dev_frames[i % len(frames)], out)
+                ev[i][1].record(stream)
+            stream.synchronize()
+        barrier()
+        launches = m.launch_count() - launches0
+        stage = m.stage_times()
+        m.set_timing(False)
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        total_ms = sum(step_ms)
+        # ---- counts for the algorithmic bytes (from the GPU's own output) --
+        lut, data, _ = m.export_frame(0)
+        H = int(data["hits"].sum())
+        Mi = int(data["misses"].sum()) + int((-1 - lut[lut < 0].astype(np.int64)).sum())
+        k = int(data["hits"].shape[0])
+        # ---- e2e: pinned host in, pinned host out ---------------------------
+        host_frames = [[(torch.from_numpy(s.points).pin_memory(), s.pose, s.rings) for s in f.scans]
+                       for f in frames]
+        host_out = {kk: torch.empty(v.shape, dtype=v.dtype).pin_memory() for kk, v in out.items()}
+        e2e_steps = max(3, min(args.steps, 100))
+        for i in range(3):
+            step(i, host_frames[i % len(frames)], host_out)
+        stream.synchronize()
+        barrier()
+        e2e_ms = 0.0
+        for i in range(e2e_steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(i, host_frames[i % len(frames)], host_out)
+            b.record(stream)
+            b.synchronize()
+            e2e_ms += a.elapsed_time(b)
+        barrier()
+
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+    pts_total = npts * args.steps * world
+    value = pts_total / (total_ms / 1e3)
+    e2e_value = npts * e2e_steps * world / (e2e_ms / 1e3)
+
+    peak, peak_src = peaks()
+    ray_ms, ray_n = stage["raycast"]
+    ray_launch_ms = ray_ms / max(ray_n, 1)
+    scans_per_frame = len(frames[0].scans)
+    pts_per_launch = npts / scans_per_frame
+    ray_bytes = (16 * npts + 8 * Mi + 8 * H) / scans_per_frame  # per launch
+    ray_gbs = ray_bytes / (ray_launch_ms / 1e3) / 1e9
+    V = m.nx * m.ny * m.nz
+    integ_keys = ("memset", "raycast", "rank_count", "rank_scan", "finalize", "endpoint")
+    integ_ms = sum(stage[s][0] for s in integ_keys) / args.steps
+    B_int = 16 * npts + 48 * H + 8 * Mi + 4 * V
+    K = int(w.grid["buffer_frames"])
+    maps_ms = sum(stage[s][0] for s in ("columns", "slope", "negative")) / args.steps
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = oracle_run(w, args.cpu_budget)
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32+int", "data": "synthetic",
+            "config": {"workload": w.name, "points_per_scan": npts, "sensors": scans_per_frame,
+                       "grid": f"{m.nx}x{m.ny}x{m.nz}@{w.grid['res']}m", "buffer_frames": K,
+                       "frames_cycled": len(frames), "l2": "flushed (256 MiB write) between steps",
+                       "step": "shift+integrate_scan+compute_maps+export_2d x7"},
+            "map_updates_per_s": world * args.steps / (total_ms / 1e3),
+            "roofline": {"bound": "hbm", "kernel": "k_raycast", "achieved": ray_gbs,
+                         "peak": peak, "unit": "GB/s", "frac": ray_gbs / peak, "traffic": None,
+                         "peak_source": peak_src, "launch_ms": ray_launch_ms,
+                         "bytes_per_launch": ray_bytes,
+                         "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)"},
+            "integrate": {"ms_per_frame": integ_ms, "points_per_s": npts / (integ_ms / 1e3),
+                          "B_int_bytes": B_int, "hbm_frac": B_int / (integ_ms / 1e3) / 1e9 / peak,
+                          "H": H, "M": Mi, "k": k},
+            "compute_maps_ms": maps_ms,
+            "stages_ms_per_step": {s: v[0] / args.steps for s, v in stage.items() if v[1]},
+            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * npts,
+                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 4 + 3), "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,196 @@
+/*
+ * gvom.h -- C ABI of the B200-native G-VOM per-scan voxel-map update.
+ *
+ * G-VOM: "a GPU accelerated voxel mapping system for off-road navigation"
+ * (arXiv 2109.13176, /root/reference/PAPER.md, cited below as P:<line>).
+ * The calls follow the paper's problem statement: "Our system requires only
+ * odometry and lidar sensor data ... [maps] can then be exported as a series
+ * of 2D maps", with a fixed-size map centred on the vehicle.
+ *
+ * Conventions:
+ *  - Every call returns gvom_status (0 = OK); nothing throws or aborts.
+ *  - Every device operation is enqueued on the handle's CUDA stream, in call
+ *    order; calls return before the GPU finishes unless stated otherwise.
+ *  - Pointers are plain host or device addresses (CUDA unified addressing
+ *    decides which).  The caller owns every buffer it passes, including the
+ *    workspace; the library allocates no device memory of its own.
+ *  - Buffers passed to a call must stay valid until the stream has passed
+ *    that call (the caller synchronises, e.g. with gvom_synchronize()).
+ *  - A handle is not thread-safe; several handles may coexist.
+ *  - Voxel units: voxel (x,y,z) of a map with origin o covers world
+ *    [(o+v)*res, (o+v+1)*res).  Linear index L = z + nz*(x + nx*y)
+ *    (z fastest, then x, then y).  2D layers are [ny][nx], x fastest.
+ */
+#ifndef GVOM_H
+#define GVOM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GVOM_API __attribute__((visibility("default")))
+#else
+#define GVOM_API
+#endif
+
+#define GVOM_ABI_VERSION 1
+#define GVOM_MAX_BUFFER_FRAMES 32
+#define GVOM_MAX_SENSORS 64
+
+typedef enum gvom_status {
+  GVOM_OK = 0,
+  GVOM_E_INVALID = -1,        /* bad argument, config or pose                         */
+  GVOM_E_NOMEM = -2,          /* workspace smaller than gvom_workspace_bytes()        */
+  GVOM_E_CUDA = -3,           /* a CUDA runtime call failed                           */
+  GVOM_E_SENSOR_OUTSIDE = -4, /* a sensor voxel is outside the grid: scan rejected,
+                                 map state unchanged (reading A9)                     */
+  GVOM_E_EMPTY = -5,          /* compute_maps / export on an empty buffer             */
+  GVOM_E_SIZE = -6            /* destination or point capacity too small              */
+} gvom_status;
+
+/* Map and layer parameters.  The paper names these but gives values only for
+ * the map size and resolution ("typically [256,256,64] with a
+ * resolution of 40 cm"); defaults are in DESIGN.md "Parameters". */
+typedef struct gvom_config {
+  int32_t nx, ny, nz;            /* voxels, each >= 1, nz <= 2048, nx*ny*nz < 2^31 */
+  double res;                    /* metres per voxel edge, > 0                    */
+  double z_center_frac;          /* vehicle z at floor(nz*frac) voxels (reading A3)      */
+  int32_t buffer_frames;         /* K per-scan maps kept ("the buffer"), 1..32       */
+  int32_t pad0;
+  int64_t max_points_per_frame;  /* capacity: points of all sensors of one frame          */
+  double min_obstacle_height;    /* metres above the surface                     */
+  double max_obstacle_height;    /* metres above the surface                     */
+  double density_threshold;      /* hard iff density >= threshold (reading A20)   */
+  int32_t slope_window;          /* N of the N x N plane fit, odd, 3..9          */
+  int32_t min_plane_points;      /* >= 3 defined cells for a fit (reading A22)           */
+  double neg_obs_threshold;      /* Delta-H in metres, flag iff larger    */
+  int32_t neg_obs_search_cells;  /* cone search distance in cells, >= 1          */
+  int32_t pad1;
+} gvom_config;
+
+/* One lidar scan of one sensor ("pointcloud and odometry data").
+ * xyzw: n points, float32 [n][4] (x, y, z, ignored) in the SENSOR frame,
+ *       16-byte aligned, host (pinned or pageable) or device memory.
+ *       Non-finite points and exact (0,0,0) no-returns are dropped (A5).
+ * sensor_to_world: 3x4 row-major [R | t] odometry pose, metres; R must be
+ *       orthonormal with det +1 within 1e-6 (else GVOM_E_INVALID).
+ * rings: points per azimuth column when the scan is in sensor order
+ *       (column-major, beam-fastest), or 0 for an unordered cloud.  Only the
+ *       work assignment uses it; results do not depend on it.            */
+typedef struct gvom_scan {
+  const float* xyzw;
+  int64_t n;
+  double sensor_to_world[12];
+  int32_t rings;
+  int32_t pad;
+} gvom_scan;
+
+/* One data-array row ("number of returns within the voxel, number of
+ * rays passing though the voxel, and the height of the lowest return").
+ * min_dz: lowest return inside the voxel in 1/65536 voxel above its floor
+ * (reading A12); m1 = sum dz, m2 = sum dz^2 over the returns (A13).      */
+typedef struct gvom_voxel {
+  uint32_t hits;
+  uint32_t misses;
+  uint32_t min_dz;
+  uint32_t reserved;
+  uint64_t m1;
+  uint64_t m2;
+} gvom_voxel;
+
+/* The 2D maps (fig:outputs P:39).  f32 layers use NaN as nodata;
+ * flag layers are uint8 0/1.  All [ny][nx], x fastest.                  */
+typedef enum gvom_layer {
+  GVOM_LAYER_HEIGHT = 0,    /* f32 metres, world z of the surface      */
+  GVOM_LAYER_DENSITY = 1,   /* f32 in [0,1], band-weighted density      */
+  GVOM_LAYER_HARD = 2,      /* u8 hard positive obstacle                */
+  GVOM_LAYER_SOFT = 3,      /* u8 soft positive obstacle                */
+  GVOM_LAYER_NEGATIVE = 4,  /* u8 negative obstacle              */
+  GVOM_LAYER_SLOPE = 5,     /* f32 radians, atan |grad| of the plane    */
+  GVOM_LAYER_ROUGHNESS = 6, /* f32 m^2, mean squared plane residual     */
+  GVOM_LAYER_COUNT = 7
+} gvom_layer;
+
+typedef struct gvom_handle gvom_handle;
+
+/* Bytes of device workspace a handle with this config needs (0 if invalid). */
+GVOM_API size_t gvom_workspace_bytes(const gvom_config* cfg);
+
+/* Create a handle over a caller-owned device workspace (>= workspace_bytes,
+ * 256-byte aligned) on CUDA stream `cuda_stream` (cudaStream_t, may be NULL
+ * for the legacy default stream).  Initialises the workspace on the stream.
+ * The initial origin is the snap of vehicle (0,0,0).                       */
+GVOM_API gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_bytes,
+                        void* cuda_stream, gvom_handle** out);
+GVOM_API gvom_status gvom_destroy(gvom_handle* h);
+GVOM_API gvom_status gvom_set_stream(gvom_handle* h, void* cuda_stream);
+GVOM_API gvom_status gvom_synchronize(gvom_handle* h);
+
+/* Re-centre the map on the vehicle ("fixed map size centered on the
+ * vehicle"; P:81 origin "always an integer multiple of the map resolution").
+ * o = floor(p/res + 0.5) - (nx/2, ny/2, floor(nz*z_center_frac)) voxels
+ * (reading A3).  Sets the origin used by subsequent integrate_scan calls;
+ * writes o_new - o_old to out_delta_voxels (may be NULL).  Host only.      */
+GVOM_API gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_delta_voxels[3]);
+
+/* Pointcloud processing: transform the scans of n_scans sensors into
+ * the map frame, bin the returns (LUT + data array), trace every ray from its
+ * sensor to its return counting pass-throughs, and insert the resulting map
+ * (LUT, data array, origin) into the buffer, evicting the oldest when K maps
+ * are held.  All sensors of one call form one buffer map (reading A15).
+ * Errors: GVOM_E_INVALID (pose, n < 0, n_scans outside 0..64),
+ * GVOM_E_SIZE (sum n > max_points_per_frame), GVOM_E_SENSOR_OUTSIDE (scan
+ * rejected, state unchanged).  n_scans = 0 pushes an empty map.    */
+GVOM_API gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans);
+
+/* Map processing: combine all buffer maps at the origin of the
+ * newest one, then compute height, density, hard, soft, slope,
+ * roughness and negative-obstacle layers.  GVOM_E_EMPTY if no map.         */
+GVOM_API gvom_status gvom_compute_maps(gvom_handle* h);
+
+/* Copy one layer of the last compute_maps into dst (host or device), which
+ * must hold nx*ny*4 bytes (f32 layers) or nx*ny bytes (u8 layers), else
+ * GVOM_E_SIZE.  Stream-ordered: synchronise before reading a host dst.     */
+GVOM_API gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes);
+
+/* World-voxel origin of the last compute_maps (newest buffer map).  */
+GVOM_API gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]);
+
+/* The combined voxel map of the last compute_maps encoded as in P:81:
+ * d_lut[V] (rank in L order if occupied, else -1 - min(N_m, 2^30)) and
+ * d_data[k] rows in L order.  Synchronous (reads k back).  Needs cap >= k
+ * (else GVOM_E_SIZE with *out_k set).  The outputs P:297 calls "the
+ * completed voxel map".                                                    */
+GVOM_API gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_data, int64_t cap,
+                               int64_t* out_k);
+
+/* One buffer map (age 0 = newest): its LUT, data rows and origin, as
+ * produced by integrate_scan.  Synchronous.                               */
+GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_voxel* d_data,
+                              int64_t cap, int64_t* out_k, int64_t out_origin[3]);
+
+/* Instrumentation.  With timing enabled every kernel launch is bracketed by
+ * CUDA events on the handle's stream; gvom_stage_times synchronises and
+ * returns, per stage, [total ms, launches] pairs (2*GVOM_STAGE_COUNT
+ * doubles), then clears the record.  gvom_launch_count returns the number of
+ * kernels this handle has launched so far.                                  */
+enum {
+  GVOM_STAGE_RAYCAST = 0, GVOM_STAGE_RANK_COUNT, GVOM_STAGE_RANK_SCAN, GVOM_STAGE_FINALIZE,
+  GVOM_STAGE_ENDPOINT, GVOM_STAGE_COLUMNS, GVOM_STAGE_SLOPE, GVOM_STAGE_NEGATIVE,
+  GVOM_STAGE_MEMSET, GVOM_STAGE_H2D, GVOM_STAGE_EXPORT, GVOM_STAGE_MERGE, GVOM_STAGE_COUNT
+};
+GVOM_API gvom_status gvom_set_timing(gvom_handle* h, int32_t enable);
+GVOM_API gvom_status gvom_stage_times(gvom_handle* h, double* out, int32_t n_doubles);
+GVOM_API int64_t gvom_launch_count(const gvom_handle* h);
+
+GVOM_API const char* gvom_status_string(gvom_status s);
+GVOM_API int32_t gvom_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVOM_H */

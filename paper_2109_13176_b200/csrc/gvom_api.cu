@@ -1,0 +1,546 @@
+// gvom_api.cu -- host side of the C ABI (include/gvom.h).
+//
+// Owns no device memory: carves the caller's workspace, validates inputs,
+// folds poses into per-sensor affines (reading A4), keeps the buffer ring of
+// per-scan maps and enqueues the kernels of k_integrate.cu and
+// k_maps.cu on the handle's stream.
+#include <math.h>
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "gvom_internal.cuh"
+
+using namespace gvom;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct Slot {
+  int32_t* lut = nullptr;
+  uint32_t* bits = nullptr;
+  uint32_t* wprefix = nullptr;
+  gvom_voxel* data = nullptr;
+  uint32_t* meta = nullptr;  // [0] = k (occupied voxels)
+  int64_t origin[3] = {0, 0, 0};
+};
+
+struct Layout {
+  size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
+  size_t staging, rank_tmp, layers_f32, layers_u8, qs, mbits, mprefix, total;
+  int64_t cap, nblk, cells;
+};
+
+bool valid_config(const gvom_config* c) {
+  if (!c) return false;
+  if (c->nx < 1 || c->ny < 1 || c->nz < 1 || c->nz > 2048) return false;
+  if ((int64_t)c->nx * c->ny * c->nz >= (1ll << 31)) return false;
+  if (!(c->res > 0) || !isfinite(c->res)) return false;
+  if (!(c->z_center_frac >= 0.0 && c->z_center_frac <= 1.0)) return false;
+  if (c->buffer_frames < 1 || c->buffer_frames > GVOM_MAX_BUFFER_FRAMES) return false;
+  if (c->max_points_per_frame < 0) return false;
+  if (!(c->min_obstacle_height >= 0) || !(c->max_obstacle_height >= c->min_obstacle_height))
+    return false;
+  if (!(c->density_threshold >= 0.0 && c->density_threshold <= 1.0)) return false;
+  if (c->slope_window < 3 || c->slope_window > 9 || (c->slope_window % 2) == 0) return false;
+  if (c->min_plane_points < 3) return false;
+  if (!(c->neg_obs_threshold >= 0) || c->neg_obs_search_cells < 1) return false;
+  return true;
+}
+
+Dims make_dims(const gvom_config* c) {
+  Dims d;
+  d.nx = c->nx;
+  d.ny = c->ny;
+  d.nz = c->nz;
+  d.V = (int64_t)c->nx * c->ny * c->nz;
+  d.W = (d.V + 31) / 32;
+  return d;
+}
+
+Layout make_layout(const gvom_config* c) {
+  Layout l{};
+  const Dims d = make_dims(c);
+  l.cap = c->max_points_per_frame < d.V ? c->max_points_per_frame : d.V;
+  l.nblk = rank_blocks(d);
+  l.cells = (int64_t)c->nx * c->ny;
+  size_t off = 0;
+  l.slot_lut = 0;
+  l.slot_bits = align_up(4 * (size_t)d.V);
+  l.slot_wprefix = l.slot_bits + align_up(4 * (size_t)d.W);
+  l.slot_data = l.slot_wprefix + align_up(4 * (size_t)d.W);
+  l.slot_meta = l.slot_data + align_up(sizeof(gvom_voxel) * (size_t)(l.cap > 0 ? l.cap : 1));
+  l.slot_stride = l.slot_meta + kAlign;
+  off = l.slot_stride * (size_t)c->buffer_frames;
+  l.staging = off;
+  off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
+  l.rank_tmp = off;
+  off += align_up(4 * (size_t)(l.nblk + 2));
+  l.layers_f32 = off;  // height, density, slope, rough
+  off += 4 * align_up(4 * (size_t)l.cells);
+  l.layers_u8 = off;  // hard, soft, neg
+  off += 3 * align_up((size_t)l.cells);
+  l.qs = off;
+  off += align_up(4 * (size_t)l.cells);
+  l.mbits = off;
+  off += align_up(4 * (size_t)d.W);
+  l.mprefix = off;
+  off += align_up(4 * (size_t)d.W);
+  l.total = off;
+  return l;
+}
+
+struct TimedRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct gvom_handle {
+  gvom_config cfg;
+  Dims d;
+  Layout lay;
+  cudaStream_t st = nullptr;
+  char* ws = nullptr;
+  std::vector<Slot> slots;
+  int K = 0, head = 0, count = 0;
+  float4* staging = nullptr;
+  uint32_t* rank_tmp = nullptr;
+  LayerPtrs layers{};
+  uint32_t* mbits = nullptr;
+  uint32_t* mprefix = nullptr;
+  LayerParams lp{};
+  int64_t origin[3] = {0, 0, 0};
+  int64_t map_origin[3] = {0, 0, 0};
+  bool maps_valid = false;
+  SlotSet map_slots{};
+  bool timing = false;
+  std::vector<TimedRec> recs;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches = 0;
+};
+
+namespace {
+
+cudaEvent_t take_event(gvom_handle* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// Run one stage (a kernel launch or a copy) with optional event timing.
+template <class F>
+cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (h->timing) {
+    a = take_event(h);
+    b = take_event(h);
+    if (a) cudaEventRecord(a, h->st);
+  }
+  const cudaError_t e = f();
+  if (h->timing && a && b) {
+    cudaEventRecord(b, h->st);
+    h->recs.push_back({id, a, b});
+  }
+  if (is_kernel && e == cudaSuccess) h->launches++;
+  return e;
+}
+
+void snap(const gvom_config& c, const double p[3], int64_t o[3]) {
+  // reading A3: o = floor(p/res + 0.5) - (nx/2, ny/2, floor(nz * frac))
+  o[0] = (int64_t)floor(p[0] / c.res + 0.5) - (int64_t)(c.nx / 2);
+  o[1] = (int64_t)floor(p[1] / c.res + 0.5) - (int64_t)(c.ny / 2);
+  o[2] = (int64_t)floor(p[2] / c.res + 0.5) - (int64_t)floor((double)c.nz * c.z_center_frac);
+}
+
+bool pose_ok(const double* P) {
+  for (int i = 0; i < 12; ++i)
+    if (!isfinite(P[i])) return false;
+  // R R^T = I within 1e-6, det(R) = +1 within 1e-6
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += P[4 * i + k] * P[4 * j + k];
+      if (fabs(s - (i == j ? 1.0 : 0.0)) > 1e-6) return false;
+    }
+  const double det = P[0] * (P[5] * P[10] - P[6] * P[9]) - P[1] * (P[4] * P[10] - P[6] * P[8]) +
+                     P[2] * (P[4] * P[9] - P[5] * P[8]);
+  return fabs(det - 1.0) <= 1e-6;
+}
+
+SensorParams sensor_params(const gvom_config& c, const double* P, const int64_t o[3]) {
+  SensorParams sp;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) sp.A[3 * i + j] = (float)(P[4 * i + j] / c.res);
+    sp.b[i] = (float)(P[4 * i + 3] / c.res - (double)o[i]);
+    sp.S[i] = (int32_t)floorf(sp.b[i]);
+  }
+  return sp;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+#define GVOM_CU(x)                                     \
+  do {                                                 \
+    if ((x) != cudaSuccess) return GVOM_E_CUDA;        \
+  } while (0)
+
+SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
+  SlotSet ss{};
+  ss.K = h->count;
+  for (int age = 0; age < h->count; ++age) {
+    const int idx = ((h->head - 1 - age) % h->K + h->K) % h->K;
+    const Slot& s = h->slots[idx];
+    SlotView& v = ss.s[age];
+    v.lut = s.lut;
+    v.bits = s.bits;
+    v.wprefix = s.wprefix;
+    v.data = s.data;
+    v.dx = (int32_t)(o_out[0] - s.origin[0]);
+    v.dy = (int32_t)(o_out[1] - s.origin[1]);
+    v.dz = (int32_t)(o_out[2] - s.origin[2]);
+    // slots shifted by a whole map extent or more contribute nothing
+    if (llabs(o_out[0] - s.origin[0]) >= h->cfg.nx || llabs(o_out[1] - s.origin[1]) >= h->cfg.ny ||
+        llabs(o_out[2] - s.origin[2]) >= h->cfg.nz) {
+      v.dx = h->cfg.nx;  // every source column out of range
+      v.dy = 0;
+      v.dz = 0;
+    }
+  }
+  return ss;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t gvom_abi_version(void) { return GVOM_ABI_VERSION; }
+
+const char* gvom_status_string(gvom_status s) {
+  switch (s) {
+    case GVOM_OK: return "ok";
+    case GVOM_E_INVALID: return "invalid argument";
+    case GVOM_E_NOMEM: return "workspace too small";
+    case GVOM_E_CUDA: return "CUDA error";
+    case GVOM_E_SENSOR_OUTSIDE: return "sensor outside the map";
+    case GVOM_E_EMPTY: return "empty map buffer";
+    case GVOM_E_SIZE: return "capacity too small";
+  }
+  return "unknown status";
+}
+
+size_t gvom_workspace_bytes(const gvom_config* cfg) {
+  if (!valid_config(cfg)) return 0;
+  return make_layout(cfg).total;
+}
+
+gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_bytes,
+                        void* cuda_stream, gvom_handle** out) {
+  if (!out) return GVOM_E_INVALID;
+  *out = nullptr;
+  if (!valid_config(cfg) || !d_workspace) return GVOM_E_INVALID;
+  if (((uintptr_t)d_workspace % kAlign) != 0) return GVOM_E_INVALID;
+  const Layout lay = make_layout(cfg);
+  if (ws_bytes < lay.total) return GVOM_E_NOMEM;
+  gvom_handle* h = new (std::nothrow) gvom_handle();
+  if (!h) return GVOM_E_NOMEM;
+  h->cfg = *cfg;
+  h->d = make_dims(cfg);
+  h->lay = lay;
+  h->st = (cudaStream_t)cuda_stream;
+  h->ws = (char*)d_workspace;
+  h->K = cfg->buffer_frames;
+  h->slots.resize(h->K);
+  for (int k = 0; k < h->K; ++k) {
+    char* b = h->ws + lay.slot_stride * (size_t)k;
+    Slot& s = h->slots[k];
+    s.lut = (int32_t*)(b + lay.slot_lut);
+    s.bits = (uint32_t*)(b + lay.slot_bits);
+    s.wprefix = (uint32_t*)(b + lay.slot_wprefix);
+    s.data = (gvom_voxel*)(b + lay.slot_data);
+    s.meta = (uint32_t*)(b + lay.slot_meta);
+  }
+  h->staging = (float4*)(h->ws + lay.staging);
+  h->rank_tmp = (uint32_t*)(h->ws + lay.rank_tmp);
+  const size_t f32 = align_up(4 * (size_t)lay.cells), u8 = align_up((size_t)lay.cells);
+  h->layers.height = (float*)(h->ws + lay.layers_f32);
+  h->layers.density = (float*)(h->ws + lay.layers_f32 + f32);
+  h->layers.slope = (float*)(h->ws + lay.layers_f32 + 2 * f32);
+  h->layers.rough = (float*)(h->ws + lay.layers_f32 + 3 * f32);
+  h->layers.hard = (uint8_t*)(h->ws + lay.layers_u8);
+  h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
+  h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
+  h->layers.qs = (int32_t*)(h->ws + lay.qs);
+  h->mbits = (uint32_t*)(h->ws + lay.mbits);
+  h->mprefix = (uint32_t*)(h->ws + lay.mprefix);
+  // integer thresholds
+  h->lp.T_lo = llround(cfg->min_obstacle_height / cfg->res * 65536.0);
+  h->lp.T_hi = llround(cfg->max_obstacle_height / cfg->res * 65536.0);
+  h->lp.tau = llround(cfg->density_threshold * 65536.0);
+  h->lp.T_neg = llround(cfg->neg_obs_threshold / cfg->res * 65536.0);
+  h->lp.res = cfg->res;
+  h->lp.slope_window = cfg->slope_window;
+  h->lp.min_plane_points = cfg->min_plane_points;
+  h->lp.neg_cells = cfg->neg_obs_search_cells;
+  const double zero[3] = {0, 0, 0};
+  snap(*cfg, zero, h->origin);
+  if (cudaMemsetAsync(h->ws, 0, lay.total, h->st) != cudaSuccess) {
+    delete h;
+    return GVOM_E_CUDA;
+  }
+  *out = h;
+  return GVOM_OK;
+}
+
+gvom_status gvom_destroy(gvom_handle* h) {
+  if (!h) return GVOM_E_INVALID;
+  for (auto& r : h->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  delete h;
+  return GVOM_OK;
+}
+
+gvom_status gvom_set_stream(gvom_handle* h, void* cuda_stream) {
+  if (!h) return GVOM_E_INVALID;
+  h->st = (cudaStream_t)cuda_stream;
+  return GVOM_OK;
+}
+
+gvom_status gvom_synchronize(gvom_handle* h) {
+  if (!h) return GVOM_E_INVALID;
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  return GVOM_OK;
+}
+
+gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_delta[3]) {
+  if (!h || !vehicle_xyz) return GVOM_E_INVALID;
+  for (int i = 0; i < 3; ++i)
+    if (!isfinite(vehicle_xyz[i])) return GVOM_E_INVALID;
+  int64_t o[3];
+  snap(h->cfg, vehicle_xyz, o);
+  if (out_delta)
+    for (int i = 0; i < 3; ++i) out_delta[i] = o[i] - h->origin[i];
+  for (int i = 0; i < 3; ++i) h->origin[i] = o[i];
+  return GVOM_OK;
+}
+
+gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
+  if (!h || n_scans < 0 || n_scans > GVOM_MAX_SENSORS || (n_scans > 0 && !scans))
+    return GVOM_E_INVALID;
+  SensorParams sp[GVOM_MAX_SENSORS];
+  int64_t total = 0;
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n < 0 || (s.n > 0 && !s.xyzw) || s.rings < 0) return GVOM_E_INVALID;
+    if (((uintptr_t)s.xyzw % 16) != 0) return GVOM_E_INVALID;
+    if (!pose_ok(s.sensor_to_world)) return GVOM_E_INVALID;
+    sp[i] = sensor_params(h->cfg, s.sensor_to_world, h->origin);
+    total += s.n;
+  }
+  if (total > h->cfg.max_points_per_frame) return GVOM_E_SIZE;
+  for (int i = 0; i < n_scans; ++i) {
+    const SensorParams& p = sp[i];
+    if ((unsigned)p.S[0] >= (unsigned)h->d.nx || (unsigned)p.S[1] >= (unsigned)h->d.ny ||
+        (unsigned)p.S[2] >= (unsigned)h->d.nz || !isfinite(p.b[0]) || !isfinite(p.b[1]) ||
+        !isfinite(p.b[2]))
+      return GVOM_E_SENSOR_OUTSIDE;
+  }
+  Slot& slot = h->slots[h->head];
+  const Dims& d = h->d;
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+    cudaError_t e = cudaMemsetAsync(slot.lut, 0, 4 * (size_t)d.V, h->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(slot.bits, 0, 4 * (size_t)d.W, h->st);
+    return e;
+  }));
+  // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
+  std::vector<const float4*> dptr(n_scans);
+  int64_t off = 0;
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n == 0) {
+      dptr[i] = nullptr;
+      continue;
+    }
+    if (is_device_ptr(s.xyzw)) {
+      dptr[i] = (const float4*)s.xyzw;
+    } else {
+      float4* dst = h->staging + off;
+      GVOM_CU(stage(h, GVOM_STAGE_H2D, false, [&] {
+        return cudaMemcpyAsync(dst, s.xyzw, 16 * (size_t)s.n, cudaMemcpyHostToDevice, h->st);
+      }));
+      dptr[i] = dst;
+      off += s.n;
+    }
+    GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
+      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits,
+                            h->st);
+    }));
+  }
+  // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_COUNT, true,
+                [&] { return launch_rank_count(slot.bits, d, h->rank_tmp, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] {
+    return launch_rank_scan(h->rank_tmp, h->lay.nblk, slot.meta, h->st);
+  }));
+  GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
+    return launch_finalize(slot.lut, slot.bits, slot.wprefix, h->rank_tmp, slot.data, d, h->st);
+  }));
+  // pass 2b: per-return metrics into the data rows
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n == 0) continue;
+    GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
+      return launch_endpoint(dptr[i], s.n, s.rings, sp[i], d, slot.lut, slot.data, h->st);
+    }));
+  }
+  for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
+  h->head = (h->head + 1) % h->K;
+  if (h->count < h->K) h->count++;
+  return GVOM_OK;
+}
+
+gvom_status gvom_compute_maps(gvom_handle* h) {
+  if (!h) return GVOM_E_INVALID;
+  if (h->count == 0) return GVOM_E_EMPTY;
+  const int newest = (h->head - 1 + h->K) % h->K;
+  int64_t o[3];
+  for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
+  h->map_slots = buffer_slots(h, o);
+  h->lp.o_z = o[2];
+  GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
+    return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st);
+  }));
+  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
+                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
+                [&] { return launch_negative(h->d, h->lp, h->layers, h->st); }));
+  for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
+  h->maps_valid = true;
+  return GVOM_OK;
+}
+
+gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes) {
+  if (!h || !dst) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  const void* src = nullptr;
+  size_t elem = 4;
+  switch (layer) {
+    case GVOM_LAYER_HEIGHT: src = h->layers.height; break;
+    case GVOM_LAYER_DENSITY: src = h->layers.density; break;
+    case GVOM_LAYER_SLOPE: src = h->layers.slope; break;
+    case GVOM_LAYER_ROUGHNESS: src = h->layers.rough; break;
+    case GVOM_LAYER_HARD: src = h->layers.hard; elem = 1; break;
+    case GVOM_LAYER_SOFT: src = h->layers.soft; elem = 1; break;
+    case GVOM_LAYER_NEGATIVE: src = h->layers.neg; elem = 1; break;
+    default: return GVOM_E_INVALID;
+  }
+  const size_t bytes = elem * (size_t)h->lay.cells;
+  if (dst_bytes < bytes) return GVOM_E_SIZE;
+  GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st);
+  }));
+  return GVOM_OK;
+}
+
+gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]) {
+  if (!h || !out_origin) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  for (int i = 0; i < 3; ++i) out_origin[i] = h->map_origin[i];
+  return GVOM_OK;
+}
+
+gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_data, int64_t cap,
+                               int64_t* out_k) {
+  if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  const Dims& d = h->d;
+  GVOM_CU(cudaMemsetAsync(h->mbits, 0, 4 * (size_t)d.W, h->st));
+  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
+                [&] { return launch_merge_bits(h->map_slots, d, h->mbits, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
+                [&] { return launch_rank_count(h->mbits, d, h->rank_tmp, h->st); }));
+  uint32_t* ktot = h->rank_tmp + h->lay.nblk;
+  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
+                [&] { return launch_rank_scan(h->rank_tmp, h->lay.nblk, ktot, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true, [&] {
+    return launch_prefix_only(h->mbits, h->mprefix, h->rank_tmp, d, h->st);
+  }));
+  uint32_t k = 0;
+  GVOM_CU(cudaMemcpyAsync(&k, ktot, 4, cudaMemcpyDeviceToHost, h->st));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  *out_k = k;
+  if ((int64_t)k > cap) return GVOM_E_SIZE;
+  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true, [&] {
+    return launch_merge_write(h->map_slots, d, h->mbits, h->mprefix, d_lut, d_data, h->st);
+  }));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  return GVOM_OK;
+}
+
+gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_voxel* d_data,
+                              int64_t cap, int64_t* out_k, int64_t out_origin[3]) {
+  if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
+  if (age < 0 || age >= h->count) return GVOM_E_EMPTY;
+  const int idx = ((h->head - 1 - age) % h->K + h->K) % h->K;
+  const Slot& s = h->slots[idx];
+  uint32_t k = 0;
+  GVOM_CU(cudaMemcpyAsync(&k, s.meta, 4, cudaMemcpyDeviceToHost, h->st));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  *out_k = k;
+  if (out_origin)
+    for (int i = 0; i < 3; ++i) out_origin[i] = s.origin[i];
+  if ((int64_t)k > cap) return GVOM_E_SIZE;
+  GVOM_CU(cudaMemcpyAsync(d_lut, s.lut, 4 * (size_t)h->d.V, cudaMemcpyDefault, h->st));
+  if (k > 0)
+    GVOM_CU(cudaMemcpyAsync(d_data, s.data, sizeof(gvom_voxel) * (size_t)k, cudaMemcpyDefault,
+                            h->st));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  return GVOM_OK;
+}
+
+gvom_status gvom_set_timing(gvom_handle* h, int32_t enable) {
+  if (!h) return GVOM_E_INVALID;
+  h->timing = enable != 0;
+  return GVOM_OK;
+}
+
+gvom_status gvom_stage_times(gvom_handle* h, double* out, int32_t n_doubles) {
+  if (!h || !out || n_doubles < 2 * GVOM_STAGE_COUNT) return GVOM_E_INVALID;
+  for (int i = 0; i < 2 * GVOM_STAGE_COUNT; ++i) out[i] = 0.0;
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  for (auto& r : h->recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      out[2 * r.stage] += ms;
+      out[2 * r.stage + 1] += 1.0;
+    }
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+  return GVOM_OK;
+}
+
+int64_t gvom_launch_count(const gvom_handle* h) { return h ? h->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// gvom_internal.cuh -- shared declarations of the CUDA path (kernels + host).
+// Independent of oracle/ (no shared code, headers or tables).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gvom.h"
+
+namespace gvom {
+
+constexpr int kRankWordsPerBlock = 1024;  // bitmask words per rank tile (32768 voxels)
+constexpr int kRankThreads = 256;         // 4 words per thread
+constexpr uint32_t kMissSat = 1u << 30;   // A11
+constexpr int32_t kQsUndef = INT32_MIN;   // undefined surface sentinel in qs[]
+
+// Per-sensor transform in voxel units (reading A4), folded on the host.
+struct SensorParams {
+  float A[9];
+  float b[3];
+  int32_t S[3];  // floor(b), the sensor voxel
+};
+
+struct Dims {
+  int32_t nx, ny, nz;
+  int64_t V;  // nx*ny*nz
+  int64_t W;  // bitmask words = ceil(V/32)
+};
+
+// One buffer map ("lookup array, data array, map origin").
+struct SlotView {
+  const int32_t* lut;
+  const uint32_t* bits;
+  const uint32_t* wprefix;
+  const gvom_voxel* data;
+  int32_t dx, dy, dz;  // o_out - o_slot  (source u = v + d)
+  int32_t pad;
+};
+
+struct SlotSet {
+  SlotView s[GVOM_MAX_BUFFER_FRAMES];
+  int32_t K;
+};
+
+struct LayerPtrs {
+  float* height;
+  float* density;
+  uint8_t* hard;
+  uint8_t* soft;
+  uint8_t* neg;
+  float* slope;
+  float* rough;
+  int32_t* qs;
+};
+
+struct LayerParams {
+  int64_t T_lo, T_hi, tau, T_neg;
+  double res;
+  int64_t o_z;
+  int32_t slope_window, min_plane_points, neg_cells;
+};
+
+// ---- launchers (each launches exactly one kernel; returns cudaError_t) ----
+cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
+                           const Dims& d, uint32_t* miss_grid, uint32_t* bits, cudaStream_t st);
+cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
+                              cudaStream_t st);
+cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
+                             cudaStream_t st);
+cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
+                            const uint32_t* block_off, gvom_voxel* data, const Dims& d,
+                            cudaStream_t st);
+cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
+                               const Dims& d, cudaStream_t st);
+cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
+                            const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st);
+cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
+                           const LayerPtrs& out, cudaStream_t st);
+cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                         cudaStream_t st);
+cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                            cudaStream_t st);
+cudaError_t launch_merge_bits(const SlotSet& ss, const Dims& d, uint32_t* mbits, cudaStream_t st);
+cudaError_t launch_merge_write(const SlotSet& ss, const Dims& d, const uint32_t* mbits,
+                               const uint32_t* mprefix, int32_t* lut, gvom_voxel* data,
+                               cudaStream_t st);
+
+inline int64_t rank_blocks(const Dims& d) {
+  return (d.W + kRankWordsPerBlock - 1) / kRankWordsPerBlock;
+}
+
+}  // namespace gvom

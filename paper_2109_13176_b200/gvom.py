@@ -1,0 +1,295 @@
+"""Thin Python binding of libgvom.so (include/gvom.h) -- argument marshalling only.
+
+Every step of the map update runs in the library's CUDA kernels.  PyTorch is
+used for device memory (the caller-owned workspace and output tensors) and
+streams.  There is no CPU fallback: if the library or a CUDA device is
+missing, construction raises.
+
+    m = GvomMap(grid_dict, max_points_per_frame=N)   # workspace on cuda:0
+    m.shift(vehicle_xyz)
+    m.integrate_scan([(points_f32_Nx4, pose_3x4, rings), ...])
+    m.compute_maps()
+    layers = m.export_layers()
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, Iterable, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import build_ext
+
+LAYERS = ("height", "density", "hard", "soft", "neg", "slope", "roughness")
+LAYER_ID = {"height": 0, "density": 1, "hard": 2, "soft": 3, "neg": 4, "slope": 5, "roughness": 6}
+LAYER_U8 = {"hard", "soft", "neg"}
+STAGES = ("raycast", "rank_count", "rank_scan", "finalize", "endpoint", "columns", "slope",
+          "negative", "memset", "h2d", "export", "merge")
+STATUS = {0: "ok", -1: "invalid argument", -2: "workspace too small", -3: "CUDA error",
+          -4: "sensor outside the map", -5: "empty map buffer", -6: "capacity too small"}
+
+
+class GvomError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class SensorOutside(GvomError):
+    pass
+
+
+class Config(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("res", C.c_double),
+                ("z_center_frac", C.c_double), ("buffer_frames", C.c_int32), ("pad0", C.c_int32),
+                ("max_points_per_frame", C.c_int64), ("min_obstacle_height", C.c_double),
+                ("max_obstacle_height", C.c_double), ("density_threshold", C.c_double),
+                ("slope_window", C.c_int32), ("min_plane_points", C.c_int32),
+                ("neg_obs_threshold", C.c_double), ("neg_obs_search_cells", C.c_int32),
+                ("pad1", C.c_int32)]
+
+
+class Scan(C.Structure):
+    _fields_ = [("xyzw", C.c_void_p), ("n", C.c_int64), ("sensor_to_world", C.c_double * 12),
+                ("rings", C.c_int32), ("pad", C.c_int32)]
+
+
+class Voxel(C.Structure):
+    _fields_ = [("hits", C.c_uint32), ("misses", C.c_uint32), ("min_dz", C.c_uint32),
+                ("reserved", C.c_uint32), ("m1", C.c_uint64), ("m2", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return build_ext.LIB
+
+
+def load_library() -> C.CDLL:
+    """Load the in-tree libgvom.so (build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise RuntimeError(f"libgvom.so not built ({path}); run __graft_entry__.build()")
+    L = C.CDLL(path)
+    P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "gvom_workspace_bytes": ([P], C.c_size_t),
+        "gvom_create": ([P, P, C.c_size_t, P, P], I32),
+        "gvom_destroy": ([P], I32),
+        "gvom_set_stream": ([P, P], I32),
+        "gvom_synchronize": ([P], I32),
+        "gvom_shift": ([P, P, P], I32),
+        "gvom_integrate_scan": ([P, P, I32], I32),
+        "gvom_compute_maps": ([P], I32),
+        "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
+        "gvom_map_origin": ([P, P], I32),
+        "gvom_export_voxels": ([P, P, P, I64, P], I32),
+        "gvom_export_frame": ([P, I32, P, P, I64, P, P], I32),
+        "gvom_set_timing": ([P, I32], I32),
+        "gvom_stage_times": ([P, P, I32], I32),
+        "gvom_launch_count": ([P], I64),
+        "gvom_status_string": ([I32], C.c_char_p),
+        "gvom_abi_version": ([], I32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_stream",
+            "gvom_synchronize", "gvom_shift", "gvom_integrate_scan", "gvom_compute_maps",
+            "gvom_export_2d", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
+            "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
+            "gvom_abi_version")
+
+
+def make_config(grid: dict, max_points_per_frame: int) -> Config:
+    c = Config()
+    c.nx, c.ny, c.nz = int(grid["nx"]), int(grid["ny"]), int(grid["nz"])
+    c.res = float(grid["res"])
+    c.z_center_frac = float(grid.get("z_center_frac", 0.5))
+    c.buffer_frames = int(grid.get("buffer_frames", 8))
+    c.max_points_per_frame = int(max_points_per_frame)
+    c.min_obstacle_height = float(grid["min_obstacle_height"])
+    c.max_obstacle_height = float(grid["max_obstacle_height"])
+    c.density_threshold = float(grid["density_threshold"])
+    c.slope_window = int(grid["slope_window"])
+    c.min_plane_points = int(grid["min_plane_points"])
+    c.neg_obs_threshold = float(grid["neg_obs_threshold"])
+    c.neg_obs_search_cells = int(grid["neg_obs_search_cells"])
+    return c
+
+
+def workspace_bytes(grid: dict, max_points_per_frame: int) -> int:
+    cfg = make_config(grid, max_points_per_frame)
+    return int(load_library().gvom_workspace_bytes(C.byref(cfg)))
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        if rc == -4:
+            raise SensorOutside(rc, what)
+        raise GvomError(rc, what)
+
+
+ScanLike = Tuple  # (points [n,4] f32 tensor/ndarray, pose [3,4], rings)
+
+
+class GvomMap:
+    """One robot-centred voxel map + its buffer of per-scan maps (a gvom_handle)."""
+
+    def __init__(self, grid: dict, max_points_per_frame: int, device="cuda",
+                 stream: Optional[torch.cuda.Stream] = None):
+        self.lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("GvomMap needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.grid = dict(grid)
+        self.cfg = make_config(grid, max_points_per_frame)
+        self.nx, self.ny, self.nz = self.cfg.nx, self.cfg.ny, self.cfg.nz
+        nbytes = int(self.lib.gvom_workspace_bytes(C.byref(self.cfg)))
+        if nbytes == 0:
+            raise GvomError(-1, "gvom_workspace_bytes (invalid config)")
+        with torch.cuda.device(self.device):
+            self.stream = stream or torch.cuda.current_stream(self.device)
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.h = C.c_void_p()
+        _check(self.lib.gvom_create(C.byref(self.cfg), C.c_void_p(self.workspace.data_ptr()),
+                                    nbytes, C.c_void_p(self.stream.cuda_stream),
+                                    C.byref(self.h)), "gvom_create")
+        self._keep = []
+
+    # -- lifecycle -----------------------------------------------------------
+    def close(self):
+        if self.h:
+            self.lib.gvom_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        _check(self.lib.gvom_set_stream(self.h, C.c_void_p(stream.cuda_stream)), "set_stream")
+
+    def synchronize(self):
+        _check(self.lib.gvom_synchronize(self.h), "gvom_synchronize")
+        self._keep.clear()
+
+    # -- the five calls ------------------------------------------------------
+    def shift(self, vehicle_xyz: Sequence[float]) -> np.ndarray:
+        p = (C.c_double * 3)(*[float(v) for v in vehicle_xyz])
+        d = (C.c_int64 * 3)()
+        _check(self.lib.gvom_shift(self.h, p, d), "gvom_shift")
+        return np.array(d[:], dtype=np.int64)
+
+    def integrate_scan(self, scans: Iterable[ScanLike]):
+        """scans: (points, pose[3,4], rings).  points: float32 [n,4] torch tensor
+        (cuda or pinned/pageable cpu) or numpy array; host points are copied by
+        the library inside the call (stream-ordered)."""
+        items = list(scans)
+        arr = (Scan * max(1, len(items)))()
+        keep = []
+        for i, it in enumerate(items):
+            pts, pose = it[0], it[1]
+            rings = int(it[2]) if len(it) > 2 else 0
+            if isinstance(pts, np.ndarray):
+                pts = torch.from_numpy(np.ascontiguousarray(pts, dtype=np.float32))
+            if pts.dtype != torch.float32 or pts.dim() != 2 or pts.shape[1] != 4:
+                raise ValueError("points must be float32 [n, 4]")
+            pts = pts.contiguous()
+            keep.append(pts)
+            arr[i].xyzw = pts.data_ptr() if pts.numel() else None
+            arr[i].n = pts.shape[0]
+            P = np.ascontiguousarray(np.asarray(pose, dtype=np.float64).reshape(12))
+            for j in range(12):
+                arr[i].sensor_to_world[j] = float(P[j])
+            arr[i].rings = rings
+        rc = self.lib.gvom_integrate_scan(self.h, arr, len(items))
+        _check(rc, "gvom_integrate_scan")
+        self._keep.append(keep)  # host buffers must live until the stream passes
+
+    def compute_maps(self):
+        _check(self.lib.gvom_compute_maps(self.h), "gvom_compute_maps")
+
+    def export_2d(self, layer: str, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        dt = torch.uint8 if layer in LAYER_U8 else torch.float32
+        if out is None:
+            out = torch.empty((self.ny, self.nx), dtype=dt, device=self.device)
+        assert out.dtype == dt and out.is_contiguous()
+        _check(self.lib.gvom_export_2d(self.h, LAYER_ID[layer], C.c_void_p(out.data_ptr()),
+                                       out.numel() * out.element_size()), f"export_2d({layer})")
+        return out
+
+    def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None) -> Dict[str, torch.Tensor]:
+        res = {}
+        for name in LAYERS:
+            res[name] = self.export_2d(name, None if out is None else out[name])
+        return res
+
+    def map_origin(self) -> np.ndarray:
+        o = (C.c_int64 * 3)()
+        _check(self.lib.gvom_map_origin(self.h, o), "gvom_map_origin")
+        return np.array(o[:], dtype=np.int64)
+
+    # -- voxel-map export (synchronous) --------------------------------------
+    def _alloc_voxels(self, cap: int):
+        V = self.nx * self.ny * self.nz
+        lut = torch.empty(V, dtype=torch.int32, device=self.device)
+        data = torch.empty((max(cap, 1), 8), dtype=torch.int32, device=self.device)  # 32 B rows
+        return lut, data
+
+    @staticmethod
+    def _split(data: torch.Tensor, k: int) -> Dict[str, np.ndarray]:
+        a = data[:k].cpu().numpy().view(np.uint32)
+        return dict(hits=a[:, 0].copy(), misses=a[:, 1].copy(), min_dz=a[:, 2].copy(),
+                    m1=a[:, 4:6].copy().view(np.uint64)[:, 0],
+                    m2=a[:, 6:8].copy().view(np.uint64)[:, 0])
+
+    def export_voxels(self) -> Tuple[np.ndarray, Dict[str, np.ndarray]]:
+        """Combined voxel map of the last compute_maps: (LUT [V] int32, data SoA)."""
+        cap = int(self.cfg.max_points_per_frame) * int(self.cfg.buffer_frames)
+        cap = min(cap, self.nx * self.ny * self.nz)
+        lut, data = self._alloc_voxels(cap)
+        k = C.c_int64()
+        _check(self.lib.gvom_export_voxels(self.h, C.c_void_p(lut.data_ptr()),
+                                           C.c_void_p(data.data_ptr()), cap, C.byref(k)),
+               "gvom_export_voxels")
+        return lut.cpu().numpy(), self._split(data, k.value)
+
+    def export_frame(self, age: int = 0):
+        """Buffer map by age (0 = newest): (LUT, data SoA, origin)."""
+        cap = min(int(self.cfg.max_points_per_frame), self.nx * self.ny * self.nz)
+        lut, data = self._alloc_voxels(cap)
+        k = C.c_int64()
+        o = (C.c_int64 * 3)()
+        _check(self.lib.gvom_export_frame(self.h, age, C.c_void_p(lut.data_ptr()),
+                                          C.c_void_p(data.data_ptr()), cap, C.byref(k), o),
+               "gvom_export_frame")
+        return lut.cpu().numpy(), self._split(data, k.value), np.array(o[:], dtype=np.int64)
+
+    # -- instrumentation -----------------------------------------------------
+    def set_timing(self, enable: bool):
+        _check(self.lib.gvom_set_timing(self.h, 1 if enable else 0), "gvom_set_timing")
+
+    def stage_times(self) -> Dict[str, Tuple[float, int]]:
+        buf = (C.c_double * (2 * len(STAGES)))()
+        _check(self.lib.gvom_stage_times(self.h, buf, len(buf)), "gvom_stage_times")
+        return {s: (buf[2 * i], int(buf[2 * i + 1])) for i, s in enumerate(STAGES)}
+
+    def launch_count(self) -> int:
+        return int(self.lib.gvom_launch_count(self.h))

@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element, on seeded synthetic workloads shaped like BASELINE.json's configs.
+
+c1 tiny (64x64x16), c2 OS1-64 single scan (256x256x64), c3 OS1-128 moving
+sequence (shift + merge + eviction), c4 3-lidar 512x512x64 at full size, plus
+edge cases: empty frames, invalid points, out-of-grid endpoints, unordered
+clouds, host-pointer inputs, rejected scans.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2109_13176_b200 import GvomMap, SensorOutside, synth
+from tests.gpu_helpers import (compare_frame, compare_layers, compare_merged, layers_np,
+                               run_sequence, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2():
+    return synth.workload(1)
+
+
+def test_c1_tiny(monkeypatch):
+    run_sequence(synth.workload(0))
+
+
+def test_c1_noise_free_and_unordered():
+    w = synth.config1(noise=False)
+    run_sequence(w)
+    run_sequence(w, rings_override=0)  # unordered cloud: same results
+
+
+def test_c2_single_scan(c2):
+    run_sequence(c2)
+
+
+def test_c2_host_pointer_input(c2):
+    run_sequence(c2, host=True, check_merged=False)
+
+
+def test_c2_buffer_of_identical_frames(c2):
+    # K = 8 copies of the same scan: merged counts are 8x, layers identical logic
+    f = c2.frames[0]
+    run_sequence(c2, frames=[f] * 10, check_every=5)
+
+
+@pytest.mark.parametrize("speed", [4.5, 12.0])
+def test_c3_motion_sequence(speed):
+    # BASELINE configs[2]: motion exercises shift + merge + eviction (K = 8)
+    w = synth.config3(speed=speed, n_frames=12, columns=1024)
+    run_sequence(w, check_every=4)
+
+
+def test_c4_three_lidars_full_size():
+    run_sequence(synth.workload(3))
+
+
+def test_empty_and_degenerate_frames(c2):
+    g = c2.grid
+    m = GvomMap(g, max_points_per_frame=1000)
+    om = O.OracleMap(g)
+    with pytest.raises(Exception):
+        m.compute_maps()  # empty buffer
+    m.shift((0, 0, 0))
+    om.shift((0, 0, 0))
+    pose = synth.pose_matrix(np.eye(3), (0.1, 0.2, 1.5))
+    # n = 0 scan -> empty map
+    m.integrate_scan([(torch.zeros((0, 4), device="cuda"), pose, 64)])
+    fm = om.integrate([(np.zeros((0, 4), np.float32), pose)])
+    compare_frame(m, fm)
+    m.compute_maps()
+    compare_layers(layers_np(m), om.compute_maps())
+    # invalid points mixed in: NaN, inf, exact zero, |g| >= 2^22, one valid
+    pts = np.array([[math.nan, 0, 0, 0], [math.inf, 1, 1, 0], [0, 0, 0, 0],
+                    [1e7, 0, 0, 0], [3.3, -2.1, -1.4, 0], [-1e6, 5, 2, 0]], np.float32)
+    m.integrate_scan([(torch.from_numpy(pts).cuda(), pose, 0)])
+    fm = om.integrate([(pts, pose)])
+    assert fm.stats["invalid"] == 4
+    compare_frame(m, fm)
+    m.compute_maps()
+    compare_layers(layers_np(m), om.compute_maps())
+    compare_merged(m, om)
+
+
+def test_sensor_outside_rejected_state_unchanged(c2):
+    f = c2.frames[0]
+    m = GvomMap(c2.grid, max_points_per_frame=f.n_points)
+    m.shift(f.vehicle_xyz)
+    m.integrate_scan([to_dev(s) for s in f.scans])
+    m.compute_maps()
+    before = layers_np(m)
+    far = synth.pose_matrix(np.eye(3), (500.0, 0.0, 0.0))
+    with pytest.raises(SensorOutside):
+        m.integrate_scan([(torch.from_numpy(f.scans[0].points).cuda(), far, 64)])
+    m.compute_maps()
+    after = layers_np(m)
+    for k in before:
+        assert np.array_equal(np.nan_to_num(before[k], nan=-7), np.nan_to_num(after[k], nan=-7))
+    lut, data, origin = m.export_frame(0)
+    assert m.export_frame(0)[0].shape == lut.shape
+
+
+def test_ragged_small_clouds():
+    # n not a multiple of rings*32; single points; rays leaving through every face
+    w = synth.workload(0)
+    g = w.grid
+    rs = np.random.default_rng(3)
+    for n, rings in ((1, 16), (17, 16), (33, 0), (1000, 7), (4097, 64)):
+        pts = rs.uniform(-30, 30, size=(n, 4)).astype(np.float32)
+        pose = synth.pose_matrix(synth.rot_zyx(0.3, 0.1, -0.05), (0.3, -0.2, 0.9))
+        m = GvomMap(g, max_points_per_frame=n)
+        om = O.OracleMap(g)
+        m.integrate_scan([(torch.from_numpy(pts).cuda(), pose, rings)])
+        fm = om.integrate([(pts, pose)])
+        compare_frame(m, fm)
+        m.compute_maps()
+        compare_layers(layers_np(m), om.compute_maps())
+
+
+def test_schedule_independence_and_determinism(c2):
+    f = c2.frames[0]
+    outs = []
+    for rings in (64, 0, 64):
+        m = GvomMap(c2.grid, max_points_per_frame=f.n_points)
+        m.shift(f.vehicle_xyz)
+        s = f.scans[0]
+        m.integrate_scan([(torch.from_numpy(s.points).cuda(), s.pose, rings)])
+        m.compute_maps()
+        lut, data, _ = m.export_frame(0)
+        outs.append((lut, data, layers_np(m)))
+    for lut, data, lay in outs[1:]:
+        assert np.array_equal(lut, outs[0][0])
+        for k in data:
+            assert np.array_equal(data[k], outs[0][1][k])
+        for k in lay:
+            assert np.array_equal(np.nan_to_num(lay[k], nan=-7),
+                                  np.nan_to_num(outs[0][2][k], nan=-7))
+
+
+def test_multi_stream_handles_independent(c2):
+    # two handles on two streams integrate different frames concurrently
+    f = c2.frames[0]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a = GvomMap(c2.grid, max_points_per_frame=f.n_points, stream=s1)
+    b = GvomMap(c2.grid, max_points_per_frame=f.n_points, stream=s2)
+    sc = f.scans[0]
+    pts = torch.from_numpy(sc.points).cuda()
+    torch.cuda.synchronize()
+    for h in (a, b):
+        h.shift(f.vehicle_xyz)
+        h.integrate_scan([(pts, sc.pose, sc.rings)])
+        h.compute_maps()
+    la, lb = layers_np(a), layers_np(b)
+    for k in la:
+        assert np.array_equal(np.nan_to_num(la[k], nan=-7), np.nan_to_num(lb[k], nan=-7))
