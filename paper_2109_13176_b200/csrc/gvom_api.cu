@@ -31,7 +31,8 @@ struct Slot {
 
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
-  size_t staging, rank_tmp, layers_f32, layers_u8, qs, mbits, mprefix, total;
+  size_t staging, rank_tmp, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
+      total;
   int64_t cap, nblk, cells;
 };
 
@@ -86,6 +87,9 @@ Layout make_layout(const gvom_config* c) {
   off += 3 * align_up((size_t)l.cells);
   l.qs = off;
   off += align_up(4 * (size_t)l.cells);
+  l.defbits = off;  // row + column defined-surface bitmasks
+  l.defbits_bytes = 4 * ((size_t)c->ny * ((c->nx + 31) / 32) + (size_t)c->nx * ((c->ny + 31) / 32));
+  off += align_up(l.defbits_bytes);
   l.mbits = off;
   off += align_up(4 * (size_t)d.W);
   l.mprefix = off;
@@ -205,6 +209,8 @@ bool is_device_ptr(const void* p) {
 SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
   SlotSet ss{};
   ss.K = h->count;
+  ss.kp_log2 = 0;
+  while ((1 << ss.kp_log2) < ss.K) ss.kp_log2++;
   for (int age = 0; age < h->count; ++age) {
     const int idx = ((h->head - 1 - age) % h->K + h->K) % h->K;
     const Slot& s = h->slots[idx];
@@ -288,6 +294,8 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
   h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
   h->layers.qs = (int32_t*)(h->ws + lay.qs);
+  h->layers.rowbits = (uint32_t*)(h->ws + lay.defbits);
+  h->layers.colbits = h->layers.rowbits + (size_t)cfg->ny * ((cfg->nx + 31) / 32);
   h->mbits = (uint32_t*)(h->ws + lay.mbits);
   h->mprefix = (uint32_t*)(h->ws + lay.mprefix);
   // integer thresholds
@@ -402,8 +410,11 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] {
     return launch_rank_scan(h->rank_tmp, h->lay.nblk, slot.meta, h->st);
   }));
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] {
+    return launch_prefix_only(slot.bits, slot.wprefix, h->rank_tmp, d, h->st);
+  }));
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
-    return launch_finalize(slot.lut, slot.bits, slot.wprefix, h->rank_tmp, slot.data, d, h->st);
+    return launch_finalize(slot.lut, slot.bits, slot.wprefix, slot.data, d, h->st);
   }));
   // pass 2b: per-return metrics into the data rows
   for (int i = 0; i < n_scans; ++i) {
@@ -427,6 +438,9 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
   h->map_slots = buffer_slots(h, o);
   h->lp.o_z = o[2];
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+    return cudaMemsetAsync(h->layers.rowbits, 0, h->lay.defbits_bytes, h->st);
+  }));
   GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
     return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st);
   }));

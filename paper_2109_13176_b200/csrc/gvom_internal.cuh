@@ -40,6 +40,7 @@ struct SlotView {
 struct SlotSet {
   SlotView s[GVOM_MAX_BUFFER_FRAMES];
   int32_t K;
+  int32_t kp_log2;  // log2 of the lanes per slot group (pow2 >= K)
 };
 
 struct LayerPtrs {
@@ -51,6 +52,8 @@ struct LayerPtrs {
   float* slope;
   float* rough;
   int32_t* qs;
+  uint32_t* rowbits;  // [ny][ceil(nx/32)] defined-surface bits along x
+  uint32_t* colbits;  // [nx][ceil(ny/32)] defined-surface bits along y
 };
 
 struct LayerParams {
@@ -67,9 +70,8 @@ cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* blo
                               cudaStream_t st);
 cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
                              cudaStream_t st);
-cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
-                            const uint32_t* block_off, gvom_voxel* data, const Dims& d,
-                            cudaStream_t st);
+cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const uint32_t* wprefix,
+                            gvom_voxel* data, const Dims& d, cudaStream_t st);
 cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
                                const Dims& d, cudaStream_t st);
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,

@@ -52,12 +52,34 @@ __device__ __forceinline__ bool transform_point(const SensorParams& sp, const fl
   return fabsf(g0) < kGLim && fabsf(g1) < kGLim && fabsf(g2) < kGLim;
 }
 
-// O5 stateless key: f32( f32( f32(V + [step>0]) - s ) * inv )
-__device__ __forceinline__ float dda_key(int v, int st, float s, float inv) {
-  return __fmul_rn(__fsub_rn(__int2float_rn(v + (st > 0 ? 1 : 0)), s), inv);
-}
-
 __device__ __forceinline__ int isign(int v) { return (v > 0) - (v < 0); }
+
+// Per-axis DDA setup (O5).  The stateless key of the oracle,
+//   key_a(V) = f32( f32( f32(V_a + [step_a>0]) - s_a ) * inv_a ),
+// is evaluated from a float edge e_a = f32(V_a + [step_a>0]) that moves by
+// exactly +-1 (integers < 2^24), so the key is bit-identical.  c_a counts the
+// steps left on the axis: min(rem_a, steps to leave the grid + 1); if the
+// last of them leaves the grid (rem_a exceeds the in-grid room) bit a of
+// `exitm` is set.  c_a > 0 <=> rem_a > 0 while the walk is in the grid, so
+// the oracle's axis gating and tie order are unchanged.
+__device__ __forceinline__ void axis_setup(int S, int E, float g, float s, int n, int stride,
+                                           int bit, float& e, float& f, float& inv, float& key,
+                                           int& c, int& dL, uint32_t& exitm) {
+  const int st = isign(E - S);
+  const int rem = abs(E - S);
+  const int room = st > 0 ? (n - 1 - S) : S;  // in-grid steps available
+  f = (float)st;
+  e = (float)(S + (st > 0 ? 1 : 0));
+  inv = 0.0f;
+  key = 0.0f;
+  if (rem > 0) {
+    inv = __frcp_rn(__fsub_rn(g, s));
+    key = __fmul_rn(__fsub_rn(e, s), inv);
+  }
+  c = rem <= room ? rem : room + 1;
+  if (rem > room) exitm |= bit;
+  dL = st * stride;
+}
 
 __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts, int64_t n,
                                                  int32_t rings, const SensorParams sp,
@@ -66,100 +88,72 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t p = point_index(tid, rings);
   const int lane = threadIdx.x & 31;
+  const float s0 = sp.b[0], s1 = sp.b[1], s2 = sp.b[2];
 
   bool active = false;
-  int v0 = 0, v1 = 0, v2 = 0, st0 = 0, st1 = 0, st2 = 0, r0 = 0, r1 = 0, r2 = 0;
-  float s0 = sp.b[0], s1 = sp.b[1], s2 = sp.b[2];
+  float e0 = 0.f, e1 = 0.f, e2 = 0.f, f0 = 0.f, f1 = 0.f, f2 = 0.f;
   float i0 = 0.f, i1 = 0.f, i2 = 0.f, k0 = 0.f, k1 = 0.f, k2 = 0.f;
-  int64_t L = 0;
-  const int64_t dLx = d.nz, dLy = (int64_t)d.nz * d.nx;
+  int c0 = 0, c1 = 0, c2 = 0, dL0 = 0, dL1 = 0, dL2 = 0;
+  uint32_t exitm = 0, L = 0;
 
   if (p < n) {
     const float4 q = __ldg(pts + p);
     float g0, g1, g2;
     if (transform_point(sp, q, g0, g1, g2)) {
-      const int e0 = (int)floorf(g0), e1 = (int)floorf(g1), e2 = (int)floorf(g2);
+      const int E0 = (int)floorf(g0), E1 = (int)floorf(g1), E2 = (int)floorf(g2);
+      const int strideY = d.nz * d.nx;
       // endpoint occupancy (O4/O6: occupied iff hits >= 1)
-      if ((unsigned)e0 < (unsigned)d.nx && (unsigned)e1 < (unsigned)d.ny &&
-          (unsigned)e2 < (unsigned)d.nz) {
-        const int64_t LE = (int64_t)e2 + dLx * e0 + dLy * e1;
+      if ((unsigned)E0 < (unsigned)d.nx && (unsigned)E1 < (unsigned)d.ny &&
+          (unsigned)E2 < (unsigned)d.nz) {
+        const uint32_t LE = (uint32_t)(E2 + d.nz * E0 + strideY * E1);
         atomicOr(bits + (LE >> 5), 1u << (LE & 31));
       }
-      v0 = sp.S[0];
-      v1 = sp.S[1];
-      v2 = sp.S[2];
-      st0 = isign(e0 - v0);
-      st1 = isign(e1 - v1);
-      st2 = isign(e2 - v2);
-      r0 = abs(e0 - v0);
-      r1 = abs(e1 - v1);
-      r2 = abs(e2 - v2);
-      if (r0 > 0) {
-        i0 = __frcp_rn(__fsub_rn(g0, s0));
-        k0 = dda_key(v0, st0, s0, i0);
-      }
-      if (r1 > 0) {
-        i1 = __frcp_rn(__fsub_rn(g1, s1));
-        k1 = dda_key(v1, st1, s1, i1);
-      }
-      if (r2 > 0) {
-        i2 = __frcp_rn(__fsub_rn(g2, s2));
-        k2 = dda_key(v2, st2, s2, i2);
-      }
-      L = (int64_t)v2 + dLx * v0 + dLy * v1;
-      active = (r0 + r1 + r2) > 0;  // the sensor voxel is in the grid (host check)
+      axis_setup(sp.S[0], E0, g0, s0, d.nx, d.nz, 1, e0, f0, i0, k0, c0, dL0, exitm);
+      axis_setup(sp.S[1], E1, g1, s1, d.ny, strideY, 2, e1, f1, i1, k1, c1, dL1, exitm);
+      axis_setup(sp.S[2], E2, g2, s2, d.nz, 1, 4, e2, f2, i2, k2, c2, dL2, exitm);
+      L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]);
+      active = (c0 | c1 | c2) != 0;  // the sensor voxel is in the grid (host check)
     }
   }
 
-  for (;;) {
-    const unsigned act = __ballot_sync(0xffffffffu, active);
-    if (act == 0u) break;
-    // Merge equal voxels of adjacent lanes: one atomic per run.
-    const uint32_t key = active ? (uint32_t)L : 0xffffffffu;
+  const bool x0 = exitm & 1u, x1 = exitm & 2u, x2 = exitm & 4u;
+  unsigned act = __ballot_sync(0xffffffffu, active);
+  while (act) {
+    // Merge equal voxels of adjacent lanes: one atomic per run of lanes.
+    const uint32_t key = active ? L : 0xffffffffu;
     const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
     const bool head = active && (lane == 0 || prev != key);
     const unsigned heads = __ballot_sync(0xffffffffu, head);
-    if (head) {
-      const unsigned after = ~((2u << lane) - 1u);  // lanes > lane
-      const unsigned boundary = (heads | ~act) & after;
-      const int next = boundary ? (__ffs(boundary) - 1) : 32;
-      atomicAdd(miss + L, (uint32_t)(next - lane));
-    }
-    if (active) {
-      // argmin over axes with remaining steps, ties to the lowest axis (O5)
-      int best = -1;
-      float bk = 0.f;
-      if (r0 > 0) {
-        best = 0;
-        bk = k0;
-      }
-      if (r1 > 0 && (best < 0 || k1 < bk)) {
-        best = 1;
-        bk = k1;
-      }
-      if (r2 > 0 && (best < 0 || k2 < bk)) best = 2;
-      bool inb;
-      if (best == 0) {
-        v0 += st0;
-        --r0;
-        L += dLx * st0;
-        k0 = dda_key(v0, st0, s0, i0);
-        inb = (unsigned)v0 < (unsigned)d.nx;
-      } else if (best == 1) {
-        v1 += st1;
-        --r1;
-        L += dLy * st1;
-        k1 = dda_key(v1, st1, s1, i1);
-        inb = (unsigned)v1 < (unsigned)d.ny;
-      } else {
-        v2 += st2;
-        --r2;
-        L += st2;
-        k2 = dda_key(v2, st2, s2, i2);
-        inb = (unsigned)v2 < (unsigned)d.nz;
-      }
-      active = inb && (r0 + r1 + r2) > 0;
-    }
+    const unsigned boundary = (heads | ~act) & (0xfffffffeu << lane);  // lanes > lane
+    const uint32_t cnt = (uint32_t)(__clz(__brev(boundary)) - lane);   // run length
+    asm volatile(
+        "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
+        "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
+        "r"(cnt), "r"((uint32_t)head)
+        : "memory");
+    // One DDA step for every lane (inactive lanes compute garbage that is
+    // never emitted: `active` only ever goes from true to false).
+    // argmin over axes with steps left, ties to the lowest axis (O5)
+    const bool p0 = c0 > 0, p1 = c1 > 0, p2 = c2 > 0;
+    const bool use1 = p1 && (!p0 || k1 < k0);
+    const float bk = use1 ? k1 : k0;
+    const bool use2 = p2 && (!(p0 || use1) || k2 < bk);
+    const bool a1 = use1 && !use2;
+    const bool a0 = !use1 && !use2;
+    e0 = a0 ? __fadd_rn(e0, f0) : e0;
+    e1 = a1 ? __fadd_rn(e1, f1) : e1;
+    e2 = use2 ? __fadd_rn(e2, f2) : e2;
+    c0 -= a0;
+    c1 -= a1;
+    c2 -= use2;
+    L += (uint32_t)(use2 ? dL2 : (a1 ? dL1 : dL0));
+    k0 = __fmul_rn(__fsub_rn(e0, s0), i0);
+    k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
+    k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
+    // an exit axis reaching 0 means the step left the grid
+    const bool out = (x0 && c0 == 0) || (x1 && c1 == 0) || (x2 && c2 == 0);
+    active = active && !out && (c0 | c1 | c2) != 0;
+    act = __ballot_sync(0xffffffffu, active);
   }
 }
 
@@ -279,56 +273,47 @@ __device__ __forceinline__ void store_prefix(uint32_t* __restrict__ wprefix, int
 
 // O6 in place: buf[L] holds the miss count; becomes rank (occupied) or
 // -1 - min(N_m, 2^30) (empty).  Occupied rows get {0, misses, 0xFFFFFFFF, 0, 0, 0}
-// for the endpoint pass to accumulate into.
-__global__ void __launch_bounds__(kRankThreads) k_finalize(int32_t* __restrict__ buf,
-                                                           const uint32_t* __restrict__ bits,
-                                                           uint32_t* __restrict__ wprefix,
-                                                           const uint32_t* __restrict__ block_off,
-                                                           gvom_voxel* __restrict__ data,
-                                                           const Dims d) {
-  __shared__ uint32_t sbits[kRankWordsPerBlock];
-  __shared__ uint32_t spre[kRankWordsPerBlock];
-  __shared__ uint32_t wsum[32];
-  tile_prefix(bits, d.W, block_off[blockIdx.x], sbits, spre, wsum);
-  store_prefix(wprefix, d.W, spre);
-  const int64_t vbase = (int64_t)blockIdx.x * kRankWordsPerBlock * 32;
-  for (int i = threadIdx.x * 4; i < kRankWordsPerBlock * 32; i += kRankThreads * 4) {
-    const int64_t L = vbase + i;
-    if (L >= d.V) break;
-    const bool vec = (L + 3 < d.V);
-    uint32_t m[4];
-    if (vec) {
-      const uint4 v = *reinterpret_cast<const uint4*>(buf + L);
-      m[0] = v.x;
-      m[1] = v.y;
-      m[2] = v.z;
-      m[3] = v.w;
-    } else {
-      for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
-    }
-    int32_t o[4];
+// for the endpoint pass to accumulate into.  One thread per 4 voxels (one
+// 16-byte load + store); rank from the absolute per-word prefix.
+__global__ void __launch_bounds__(256) k_finalize(int32_t* __restrict__ buf,
+                                                  const uint32_t* __restrict__ bits,
+                                                  const uint32_t* __restrict__ wprefix,
+                                                  gvom_voxel* __restrict__ data, const Dims d) {
+  const int64_t L = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (L >= d.V) return;
+  const uint32_t bw = __ldg(bits + (L >> 5));
+  const uint32_t pre = __ldg(wprefix + (L >> 5));
+  const bool vec = (L + 3 < d.V);
+  uint32_t m[4];
+  if (vec) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(buf + L));
+    m[0] = v.x;
+    m[1] = v.y;
+    m[2] = v.z;
+    m[3] = v.w;
+  } else {
+    for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
+  }
+  int32_t o[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int l = i + j;
-      const uint32_t bw = sbits[l >> 5];
-      const int bit = l & 31;
-      if ((bw >> bit) & 1u) {
-        const uint32_t rank = spre[l >> 5] + __popc(bw & ((1u << bit) - 1u));
-        o[j] = (int32_t)rank;
-        uint4* row = reinterpret_cast<uint4*>(data + rank);
-        row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
-        row[1] = make_uint4(0u, 0u, 0u, 0u);
-      } else {
-        const uint32_t nm = m[j] < kMissSat ? m[j] : kMissSat;
-        o[j] = -1 - (int32_t)nm;
-      }
-    }
-    if (vec) {
-      *reinterpret_cast<int4*>(buf + L) = make_int4(o[0], o[1], o[2], o[3]);
+  for (int j = 0; j < 4; ++j) {
+    const int bit = (int)((L + j) & 31);
+    if ((bw >> bit) & 1u) {
+      const uint32_t rank = pre + __popc(bw & ((1u << bit) - 1u));
+      o[j] = (int32_t)rank;
+      uint4* row = reinterpret_cast<uint4*>(data + rank);
+      row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
+      row[1] = make_uint4(0u, 0u, 0u, 0u);
     } else {
-      for (int j = 0; j < 4; ++j)
-        if (L + j < d.V) buf[L + j] = o[j];
+      const uint32_t nm = m[j] < kMissSat ? m[j] : kMissSat;
+      o[j] = -1 - (int32_t)nm;
     }
+  }
+  if (vec) {
+    *reinterpret_cast<int4*>(buf + L) = make_int4(o[0], o[1], o[2], o[3]);
+  } else {
+    for (int j = 0; j < 4; ++j)
+      if (L + j < d.V) buf[L + j] = o[j];
   }
 }
 
@@ -402,11 +387,11 @@ cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total
   return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
-                            const uint32_t* block_off, gvom_voxel* data, const Dims& d,
-                            cudaStream_t st) {
-  k_finalize<<<(unsigned)rank_blocks(d), kRankThreads, 0, st>>>(lut_inplace, bits, wprefix,
-                                                                 block_off, data, d);
+cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const uint32_t* wprefix,
+                            gvom_voxel* data, const Dims& d, cudaStream_t st) {
+  const int64_t threads = (d.V + 3) / 4;
+  k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(lut_inplace, bits, wprefix, data,
+                                                                d);
   return cudaGetLastError();
 }
 

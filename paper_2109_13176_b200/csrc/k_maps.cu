@@ -71,73 +71,171 @@ __device__ __forceinline__ Merged merge_voxel(const SlotSet& ss, const Dims& d, 
   return m;
 }
 
-__global__ void __launch_bounds__(128) k_columns(const SlotSet ss, const Dims d,
+// Segmented (within groups of 2^lg lanes) reductions.
+__device__ __forceinline__ uint32_t grp_or(uint32_t v, int lg) {
+  for (int o = 1; o < (1 << lg); o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t grp_add64(uint64_t v, int lg) {
+  for (int o = 1; o < (1 << lg); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t grp_min(uint32_t v, int lg) {
+  for (int o = 1; o < (1 << lg); o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// O7 + O8 fused, one warp per output column.  Lane (g, k): slot k = lane mod
+// 2^lg of group g = lane >> lg.  Groups scan different 32-z chunks, then
+// evaluate different candidate voxels of the column in parallel; each voxel is
+// the sum / min over the slots of its group (segmented shuffles).
+__global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
                                                  const LayerParams lp, const LayerPtrs out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)d.nx * d.ny) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= (int64_t)d.nx * d.ny) return;  // warp-uniform
   const int x = (int)(c % d.nx), y = (int)(c / d.nx);
-  // z*: lowest z occupied in any buffer map (O8)
+  const int lg = ss.kp_log2;
+  const int k = lane & ((1 << lg) - 1);
+  const int g = lane >> lg;
+  const int G = 32 >> lg;
+  // this lane's slot column
+  bool col = false;
+  int64_t cb = 0;
+  int dz = 0;
+  const uint32_t* bits = nullptr;
+  const uint32_t* wpre = nullptr;
+  const gvom_voxel* data = nullptr;
+  const int32_t* lut = nullptr;
+  if (k < ss.K) {
+    const SlotView& s = ss.s[k];
+    const int sx = x + s.dx, sy = y + s.dy;
+    if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny) {
+      col = true;
+      cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
+      dz = s.dz;
+      bits = s.bits;
+      wpre = s.wprefix;
+      data = s.data;
+      lut = s.lut;
+    }
+  }
+  // ---- z*: lowest z occupied in any buffer map ----
   int zs = -1;
-  for (int z0 = 0; z0 < d.nz && zs < 0; z0 += 32) {
-    uint32_t m = 0;
-    for (int k = 0; k < ss.K; ++k) {
-      const SlotView& s = ss.s[k];
-      const int sx = x + s.dx, sy = y + s.dy;
-      if ((unsigned)sx >= (unsigned)d.nx || (unsigned)sy >= (unsigned)d.ny) continue;
-      const int64_t cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
-      m |= col_bits32(s.bits, d.W, cb, z0 + s.dz, d.nz);
+  for (int zb = 0; zb < d.nz && zs < 0; zb += 32 * G) {
+    const int z0 = zb + 32 * g;
+    uint32_t m = (col && z0 < d.nz) ? col_bits32(bits, d.W, cb, z0 + dz, d.nz) : 0u;
+    m = grp_or(m, lg);
+    const unsigned nzg = __ballot_sync(0xffffffffu, m != 0u && k == 0);
+    if (nzg) {
+      const int gl = __ffs(nzg) - 1;  // leader lane of the lowest non-empty chunk
+      const uint32_t mm = __shfl_sync(0xffffffffu, m, gl);
+      zs = zb + 32 * (gl >> lg) + __ffs(mm) - 1;
     }
-    if (m) zs = z0 + __ffs(m) - 1;
   }
-  out.hard[c] = 0;
-  out.soft[c] = 0;
   if (zs < 0) {
-    out.height[c] = __int_as_float(0x7fc00000);
-    out.density[c] = __int_as_float(0x7fc00000);
-    out.qs[c] = kQsUndef;
+    if (lane == 0) {
+      out.hard[c] = 0;
+      out.soft[c] = 0;
+      out.height[c] = __int_as_float(0x7fc00000);
+      out.density[c] = __int_as_float(0x7fc00000);
+      out.qs[c] = kQsUndef;
+    }
     return;
   }
-  const Merged ms = merge_voxel(ss, d, x, y, zs);
-  const int64_t q_s = 65536ll * zs + (int64_t)ms.mn;
-  out.qs[c] = (int32_t)q_s;
-  out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
-  // obstacle band: occupied z with T_lo <= 65536 z + mn(z) - q_s <= T_hi (A18)
-  const int64_t zhi64 = (lp.T_hi + q_s) >> 16;
-  const int zhi = (int)(zhi64 < (int64_t)d.nz - 1 ? zhi64 : (int64_t)d.nz - 1);
+  // ---- candidates: merged occupancy in a window starting at z* ----
+  const int span = (int)((lp.T_hi >> 16) + 1);  // band top is at most z* + span
+  int64_t q_s = 0;
+  int zhi = zs;
   uint64_t SH = 0, SW = 0;
-  for (int z0 = zs & ~31; z0 <= zhi; z0 += 32) {
-    uint32_t m = 0;
-    for (int k = 0; k < ss.K; ++k) {
-      const SlotView& s = ss.s[k];
-      const int sx = x + s.dx, sy = y + s.dy;
-      if ((unsigned)sx >= (unsigned)d.nx || (unsigned)sy >= (unsigned)d.ny) continue;
-      const int64_t cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
-      m |= col_bits32(s.bits, d.W, cb, z0 + s.dz, d.nz);
+  bool have_qs = false;
+  for (int w0 = zs; w0 <= zs + span && w0 < d.nz; w0 += 32) {
+    uint32_t wm = col ? col_bits32(bits, d.W, cb, w0 + dz, d.nz) : 0u;
+    wm = grp_or(wm, lg);  // identical in every group
+    if (have_qs) {
+      const int lim = zhi - w0;  // keep z <= zhi
+      if (lim < 0) break;
+      if (lim < 31) wm &= (2u << lim) - 1u;
     }
-    // keep z in (zs, zhi]: the surface voxel itself has dq = mn(zs) - mn(zs) = 0
-    // which is in the band only if T_lo <= 0; handle it explicitly below.
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      const int z = z0 + b;
-      if (z < zs || z > zhi) continue;
-      const Merged mz = (z == zs) ? ms : merge_voxel(ss, d, x, y, z);
-      const int64_t dq = (65536ll * z + (int64_t)mz.mn) - q_s;
-      if (dq >= lp.T_lo && dq <= lp.T_hi) {
-        SH += mz.H;
-        SW += mz.H + mz.Mi;
+    while (wm) {
+      // group g takes the g-th remaining candidate of this batch
+      uint32_t t = wm;
+      for (int i = 0; i < g && t; ++i) t &= t - 1;
+      const bool has = t != 0u;
+      const int z = has ? w0 + __ffs(t) - 1 : -1;
+      // remove G candidates from wm
+      for (int i = 0; i < G && wm; ++i) wm &= wm - 1;
+      uint32_t h = 0, mi = 0, mn = 0xffffffffu;
+      if (has && col) {
+        const int uz = z + dz;
+        if ((unsigned)uz < (unsigned)d.nz) {
+          const int64_t L = cb + uz;
+          const int64_t wi = L >> 5;
+          const int bit = (int)(L & 31);
+          const uint32_t bw = __ldg(bits + wi);
+          if ((bw >> bit) & 1u) {
+            const uint32_t r = __ldg(wpre + wi) + __popc(bw & ((1u << bit) - 1u));
+            const uint4 row = __ldg(reinterpret_cast<const uint4*>(data + r));
+            h = row.x;
+            mi = row.y;
+            mn = row.z;
+          } else {
+            mi = (uint32_t)(-1 - __ldg(lut + L));
+          }
+        }
       }
+      const uint64_t H = grp_add64(h, lg);
+      const uint64_t Mi = grp_add64(mi, lg);
+      const uint32_t MN = grp_min(mn, lg);
+      if (!have_qs) {
+        // the first candidate of the first batch (group 0) is z* itself
+        const uint32_t mn0 = __shfl_sync(0xffffffffu, MN, 0);
+        q_s = 65536ll * zs + (int64_t)mn0;
+        const int64_t zh = (lp.T_hi + q_s) >> 16;
+        zhi = (int)(zh < (int64_t)d.nz - 1 ? zh : (int64_t)d.nz - 1);
+        have_qs = true;
+      }
+      if (k == 0 && has && z <= zhi) {
+        const int64_t dq = (65536ll * z + (int64_t)MN) - q_s;
+        if (dq >= lp.T_lo && dq <= lp.T_hi) {
+          SH += H;
+          SW += H + Mi;
+        }
+      }
+      // drop candidates above zhi (uniform: zhi and wm are warp-uniform)
+      const int lim = zhi - w0;
+      if (lim < 0)
+        wm = 0u;
+      else if (lim < 31)
+        wm &= (2u << lim) - 1u;
     }
+    // (uniform) stop once past zhi
+    if (w0 + 32 > zhi) break;
   }
-  if (SH == 0) {
-    out.density[c] = 0.0f;
-    return;
+  // sum the group leaders' partial band sums (non-leaders hold 0)
+  for (int o = 16; o > 0; o >>= 1) {
+    SH += __shfl_xor_sync(0xffffffffu, SH, o);
+    SW += __shfl_xor_sync(0xffffffffu, SW, o);
   }
-  out.density[c] = (float)((double)SH / (double)SW);
-  if (65536ull * SH >= (uint64_t)lp.tau * SW)
-    out.hard[c] = 1;
-  else
-    out.soft[c] = 1;
+  if (lane == 0) {
+    out.qs[c] = (int32_t)q_s;
+    out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
+    uint8_t hard = 0, soft = 0;
+    if (SH == 0) {
+      out.density[c] = 0.0f;
+    } else {
+      out.density[c] = (float)((double)SH / (double)SW);
+      if (65536ull * SH >= (uint64_t)lp.tau * SW)
+        hard = 1;
+      else
+        soft = 1;
+    }
+    out.hard[c] = hard;
+    out.soft[c] = soft;
+    const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
+    atomicOr(out.rowbits + (int64_t)y * WX + (x >> 5), 1u << (x & 31));
+    atomicOr(out.colbits + (int64_t)x * WY + (y >> 5), 1u << (y & 31));
+  }
 }
 
 __device__ __forceinline__ int64_t det3(int64_t a, int64_t b, int64_t c, int64_t d, int64_t e,
@@ -216,7 +314,33 @@ __global__ void __launch_bounds__(128) k_slope(const Dims d, const LayerParams l
   out.rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
 }
 
-// O10: negative obstacles for undefined cells
+// Defined cells of one ring line (a row or column segment [lo, hi]) from the
+// defined-surface bitmask; for each, fold q into (min, max, count).
+__device__ __forceinline__ bool ring_line(const uint32_t* __restrict__ bm, int lo, int hi,
+                                          const int32_t* __restrict__ qs, int64_t q0,
+                                          int64_t qstride, int64_t& fmin, int64_t& fmax,
+                                          int64_t& fcount) {
+  bool found = false;
+  for (int wi = lo >> 5; wi <= (hi >> 5); ++wi) {
+    uint32_t w = __ldg(bm + wi);
+    const int b0 = wi << 5;
+    if (lo > b0) w &= ~0u << (lo - b0);
+    if (hi < b0 + 31) w &= (2u << (hi - b0)) - 1u;
+    while (w) {
+      const int i = b0 + __ffs(w) - 1;
+      w &= w - 1;
+      const int64_t q = __ldg(qs + q0 + qstride * i);
+      fmin = min(fmin, q);
+      fmax = max(fmax, q);
+      ++fcount;
+      found = true;
+    }
+  }
+  return found;
+}
+
+// O10: negative obstacles for undefined cells.  Ring k of cone +x is
+// the column segment x+k, y-k..y+k: tested 32 cells per bitmask word.
 __global__ void __launch_bounds__(128) k_negative(const Dims d, const LayerParams lp,
                                                   const LayerPtrs out) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -227,33 +351,26 @@ __global__ void __launch_bounds__(128) k_negative(const Dims d, const LayerParam
     out.neg[c] = 0;
     return;
   }
+  const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
   int64_t fmin = INT64_MAX, fmax = INT64_MIN, fcount = 0;
   for (int cone = 0; cone < 4; ++cone) {
+    const bool alongx = cone < 2;  // +x / -x cones: ring lines are columns
+    const int sgn = (cone & 1) ? -1 : 1;
+    const int base = alongx ? x : y;
+    const int nline = alongx ? d.nx : d.ny;
+    const int center = alongx ? y : x;
+    const int lim = alongx ? d.ny : d.nx;
     for (int k = 1; k <= lp.neg_cells; ++k) {
-      bool found = false;
-      for (int t = -k; t <= k; ++t) {
-        int xx, yy;
-        if (cone == 0) {
-          xx = x + k;
-          yy = y + t;
-        } else if (cone == 1) {
-          xx = x - k;
-          yy = y + t;
-        } else if (cone == 2) {
-          xx = x + t;
-          yy = y + k;
-        } else {
-          xx = x + t;
-          yy = y - k;
-        }
-        if ((unsigned)xx >= (unsigned)d.nx || (unsigned)yy >= (unsigned)d.ny) continue;
-        const int32_t q = __ldg(qs + xx + (int64_t)d.nx * yy);
-        if (q == kQsUndef) continue;
-        found = true;
-        fmin = min(fmin, (int64_t)q);
-        fmax = max(fmax, (int64_t)q);
-        ++fcount;
-      }
+      const int line = base + sgn * k;
+      if ((unsigned)line >= (unsigned)nline) break;  // further rings are outside too
+      const int lo = max(0, center - k), hi = min(lim - 1, center + k);
+      bool found;
+      if (alongx)
+        found = ring_line(out.colbits + (int64_t)line * WY, lo, hi, qs, line, d.nx, fmin, fmax,
+                          fcount);
+      else
+        found = ring_line(out.rowbits + (int64_t)line * WX, lo, hi, qs, (int64_t)d.nx * line, 1,
+                          fmin, fmax, fcount);
       if (found) break;
     }
   }
@@ -345,7 +462,8 @@ inline unsigned cells_blocks(const Dims& d, int tpb) {
 
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
                            const LayerPtrs& out, cudaStream_t st) {
-  k_columns<<<cells_blocks(d, 128), 128, 0, st>>>(ss, d, lp, out);
+  const int64_t warps = (int64_t)d.nx * d.ny;
+  k_columns<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(ss, d, lp, out);
   return cudaGetLastError();
 }
 
