@@ -157,6 +157,13 @@ GVOM_API gvom_status gvom_compute_maps(gvom_handle* h);
  * GVOM_E_SIZE.  Stream-ordered: synchronise before reading a host dst.     */
 GVOM_API gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes);
 
+/* All seven layers at once ("each of these maps are published"):
+ * dst[l] / dst_bytes[l] for l = GVOM_LAYER_HEIGHT..GVOM_LAYER_ROUGHNESS, each
+ * as in gvom_export_2d.  When every dst is 16-byte aligned device memory the
+ * copy is one kernel launch; otherwise one async copy per layer.           */
+GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
+                                        const size_t dst_bytes[GVOM_LAYER_COUNT]);
+
 /* World-voxel origin of the last compute_maps (newest buffer map).  */
 GVOM_API gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]);
 

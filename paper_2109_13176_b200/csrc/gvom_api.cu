@@ -31,7 +31,7 @@ struct Slot {
 
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
-  size_t staging, rank_tmp, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
+  size_t staging, rank_tmp, rank_status, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
       total;
   int64_t cap, nblk, cells;
 };
@@ -81,6 +81,8 @@ Layout make_layout(const gvom_config* c) {
   off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
   l.rank_tmp = off;
   off += align_up(4 * (size_t)(l.nblk + 2));
+  l.rank_status = off;  // [0] ticket counter, [1 + b] tile status (decoupled look-back)
+  off += align_up(8 * (size_t)(l.nblk + 1));
   l.layers_f32 = off;  // height, density, slope, rough
   off += 4 * align_up(4 * (size_t)l.cells);
   l.layers_u8 = off;  // hard, soft, neg
@@ -127,6 +129,7 @@ struct gvom_handle {
   std::vector<TimedRec> recs;
   std::vector<cudaEvent_t> pool;
   int64_t launches = 0;
+  uint64_t rank_calls = 0;  // decoupled look-back epochs / ticket base
 };
 
 namespace {
@@ -205,6 +208,19 @@ bool is_device_ptr(const void* p) {
   do {                                                 \
     if ((x) != cudaSuccess) return GVOM_E_CUDA;        \
   } while (0)
+
+// rank of the occupied voxels of `bits` -> absolute per-word prefix; k -> *total
+cudaError_t run_rank(gvom_handle* h, const uint32_t* bits, uint32_t* wprefix, uint32_t* total) {
+  uint64_t* st = (uint64_t*)(h->ws + h->lay.rank_status);
+  const uint64_t call = h->rank_calls++;
+  const uint32_t epoch = (uint32_t)((call % 0x7ffffffeull) + 1);
+  if (epoch == 1 && call > 0) {  // epoch wrapped: clear stale tile status
+    cudaError_t e = cudaMemsetAsync(st + 1, 0, 8 * (size_t)h->lay.nblk, h->st);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_rank(bits, h->d, wprefix, st + 1, (unsigned long long*)st,
+                     call * (uint64_t)h->lay.nblk, epoch, total, h->st);
+}
 
 SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
   SlotSet ss{};
@@ -375,10 +391,9 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   }
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
-  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
-    cudaError_t e = cudaMemsetAsync(slot.lut, 0, 4 * (size_t)d.V, h->st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(slot.bits, 0, 4 * (size_t)d.W, h->st);
-    return e;
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
+    return launch_zero2(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
+                        (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->st);
   }));
   // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
   std::vector<const float4*> dptr(n_scans);
@@ -405,14 +420,8 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     }));
   }
   // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
-  GVOM_CU(stage(h, GVOM_STAGE_RANK_COUNT, true,
-                [&] { return launch_rank_count(slot.bits, d, h->rank_tmp, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] {
-    return launch_rank_scan(h->rank_tmp, h->lay.nblk, slot.meta, h->st);
-  }));
-  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] {
-    return launch_prefix_only(slot.bits, slot.wprefix, h->rank_tmp, d, h->st);
-  }));
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true,
+                [&] { return run_rank(h, slot.bits, slot.wprefix, slot.meta); }));
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
     return launch_finalize(slot.lut, slot.bits, slot.wprefix, slot.data, d, h->st);
   }));
@@ -453,21 +462,54 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   return GVOM_OK;
 }
 
+static const void* layer_src(gvom_handle* h, int layer, size_t* elem) {
+  *elem = 4;
+  switch (layer) {
+    case GVOM_LAYER_HEIGHT: return h->layers.height;
+    case GVOM_LAYER_DENSITY: return h->layers.density;
+    case GVOM_LAYER_SLOPE: return h->layers.slope;
+    case GVOM_LAYER_ROUGHNESS: return h->layers.rough;
+    case GVOM_LAYER_HARD: *elem = 1; return h->layers.hard;
+    case GVOM_LAYER_SOFT: *elem = 1; return h->layers.soft;
+    case GVOM_LAYER_NEGATIVE: *elem = 1; return h->layers.neg;
+    default: return nullptr;
+  }
+}
+
+gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
+                               const size_t dst_bytes[GVOM_LAYER_COUNT]) {
+  if (!h || !dst || !dst_bytes) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  CopyJob job;
+  bool one_kernel = true;
+  for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
+    size_t elem;
+    job.src[l] = layer_src(h, l, &elem);
+    job.dst[l] = dst[l];
+    job.bytes[l] = (int64_t)(elem * (size_t)h->lay.cells);
+    if (!dst[l]) return GVOM_E_INVALID;
+    if (dst_bytes[l] < (size_t)job.bytes[l]) return GVOM_E_SIZE;
+    if (((uintptr_t)dst[l] & 15) != 0 || !is_device_ptr(dst[l])) one_kernel = false;
+  }
+  if (one_kernel) {
+    GVOM_CU(stage(h, GVOM_STAGE_EXPORT, true, [&] { return launch_export_layers(job, h->st); }));
+    return GVOM_OK;
+  }
+  for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
+    GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
+      return cudaMemcpyAsync(job.dst[l], job.src[l], (size_t)job.bytes[l], cudaMemcpyDefault,
+                             h->st);
+    }));
+  }
+  return GVOM_OK;
+}
+
 gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes) {
   if (!h || !dst) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
-  const void* src = nullptr;
-  size_t elem = 4;
-  switch (layer) {
-    case GVOM_LAYER_HEIGHT: src = h->layers.height; break;
-    case GVOM_LAYER_DENSITY: src = h->layers.density; break;
-    case GVOM_LAYER_SLOPE: src = h->layers.slope; break;
-    case GVOM_LAYER_ROUGHNESS: src = h->layers.rough; break;
-    case GVOM_LAYER_HARD: src = h->layers.hard; elem = 1; break;
-    case GVOM_LAYER_SOFT: src = h->layers.soft; elem = 1; break;
-    case GVOM_LAYER_NEGATIVE: src = h->layers.neg; elem = 1; break;
-    default: return GVOM_E_INVALID;
-  }
+  size_t elem;
+  const void* src = layer_src(h, (int)layer, &elem);
+  if (!src) return GVOM_E_INVALID;
   const size_t bytes = elem * (size_t)h->lay.cells;
   if (dst_bytes < bytes) return GVOM_E_SIZE;
   GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
@@ -491,14 +533,9 @@ gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_dat
   GVOM_CU(cudaMemsetAsync(h->mbits, 0, 4 * (size_t)d.W, h->st));
   GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
                 [&] { return launch_merge_bits(h->map_slots, d, h->mbits, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
-                [&] { return launch_rank_count(h->mbits, d, h->rank_tmp, h->st); }));
   uint32_t* ktot = h->rank_tmp + h->lay.nblk;
   GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
-                [&] { return launch_rank_scan(h->rank_tmp, h->lay.nblk, ktot, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_MERGE, true, [&] {
-    return launch_prefix_only(h->mbits, h->mprefix, h->rank_tmp, d, h->st);
-  }));
+                [&] { return run_rank(h, h->mbits, h->mprefix, ktot); }));
   uint32_t k = 0;
   GVOM_CU(cudaMemcpyAsync(&k, ktot, 4, cudaMemcpyDeviceToHost, h->st));
   GVOM_CU(cudaStreamSynchronize(h->st));

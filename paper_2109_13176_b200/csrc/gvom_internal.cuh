@@ -72,6 +72,11 @@ cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total
                              cudaStream_t st);
 cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const uint32_t* wprefix,
                             gvom_voxel* data, const Dims& d, cudaStream_t st);
+cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
+                        unsigned long long* ticket, uint64_t base, uint32_t epoch,
+                        uint32_t* total, cudaStream_t st);
+// zeroes a[0:abytes) and b[0:bbytes) (sizes multiples of 16, 16-byte aligned)
+cudaError_t launch_zero2(void* a, size_t abytes, void* b, size_t bbytes, cudaStream_t st);
 cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
                                const Dims& d, cudaStream_t st);
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
@@ -86,6 +91,13 @@ cudaError_t launch_merge_bits(const SlotSet& ss, const Dims& d, uint32_t* mbits,
 cudaError_t launch_merge_write(const SlotSet& ss, const Dims& d, const uint32_t* mbits,
                                const uint32_t* mprefix, int32_t* lut, gvom_voxel* data,
                                cudaStream_t st);
+
+struct CopyJob {
+  const void* src[GVOM_LAYER_COUNT];
+  void* dst[GVOM_LAYER_COUNT];
+  int64_t bytes[GVOM_LAYER_COUNT];
+};
+cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st);
 
 inline int64_t rank_blocks(const Dims& d) {
   return (d.W + kRankWordsPerBlock - 1) / kRankWordsPerBlock;

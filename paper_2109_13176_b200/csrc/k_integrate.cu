@@ -10,6 +10,8 @@
 // the order of SURVEY.md 8(c) O3/O5, and the file is built with -fmad=false, so
 // the voxel walk is bit-identical to the oracle's.  Integer accumulation only
 // (u32/u64 atomics): results are independent of thread schedule.
+#include <cuda/atomic>
+
 #include "gvom_internal.cuh"
 
 namespace gvom {
@@ -52,32 +54,65 @@ __device__ __forceinline__ bool transform_point(const SensorParams& sp, const fl
   return fabsf(g0) < kGLim && fabsf(g1) < kGLim && fabsf(g2) < kGLim;
 }
 
-__device__ __forceinline__ int isign(int v) { return (v > 0) - (v < 0); }
+// Exact O5 walk of one ray, oracle control flow verbatim (slow path for the
+// astronomically rare rays whose reciprocal 1/d_a is not finite, where the
+// fast path's +inf-key gating would not be equivalent).
+__device__ void walk_exact(const int S[3], const int E[3], const float g[3], const float s[3],
+                           const Dims& d, uint32_t* __restrict__ miss) {
+  int V[3] = {S[0], S[1], S[2]}, st[3], rem[3];
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    st[a] = (E[a] > S[a]) - (E[a] < S[a]);
+    rem[a] = abs(E[a] - S[a]);
+    inv[a] = rem[a] > 0 ? __frcp_rn(__fsub_rn(g[a], s[a])) : 0.0f;
+  }
+  const int n[3] = {d.nx, d.ny, d.nz};
+  while ((unsigned)V[0] < (unsigned)n[0] && (unsigned)V[1] < (unsigned)n[1] &&
+         (unsigned)V[2] < (unsigned)n[2] && rem[0] + rem[1] + rem[2] > 0) {
+    atomicAdd(miss + (V[2] + d.nz * (V[0] + d.nx * V[1])), 1u);
+    int best = -1;
+    float bk = 0.f;
+    for (int a = 0; a < 3; ++a) {
+      if (rem[a] <= 0) continue;
+      const float key =
+          __fmul_rn(__fsub_rn(__int2float_rn(V[a] + (st[a] > 0 ? 1 : 0)), s[a]), inv[a]);
+      if (best < 0 || key < bk) {
+        best = a;
+        bk = key;
+      }
+    }
+    V[best] += st[best];
+    rem[best] -= 1;
+  }
+}
 
 // Per-axis DDA setup (O5).  The stateless key of the oracle,
 //   key_a(V) = f32( f32( f32(V_a + [step_a>0]) - s_a ) * inv_a ),
 // is evaluated from a float edge e_a = f32(V_a + [step_a>0]) that moves by
-// exactly +-1 (integers < 2^24), so the key is bit-identical.  c_a counts the
-// steps left on the axis: min(rem_a, steps to leave the grid + 1); if the
-// last of them leaves the grid (rem_a exceeds the in-grid room) bit a of
-// `exitm` is set.  c_a > 0 <=> rem_a > 0 while the walk is in the grid, so
-// the oracle's axis gating and tie order are unchanged.
+// exactly +-1 (integers < 2^24), so it is bit-identical.  Gating: an axis
+// with no steps left carries key +inf; with every live key finite this picks
+// exactly the oracle's argmin (strict <, ties to the lowest axis).
+//   exit axis (the walk leaves the grid through it): c = in-grid steps left;
+//   selecting it with c == 0 ends the walk.
+//   other axes: c = rem; the key becomes +inf when c reaches 0.
 __device__ __forceinline__ void axis_setup(int S, int E, float g, float s, int n, int stride,
-                                           int bit, float& e, float& f, float& inv, float& key,
-                                           int& c, int& dL, uint32_t& exitm) {
-  const int st = isign(E - S);
-  const int rem = abs(E - S);
+                                           float& e, float& f, float& inv, float& key, int& c,
+                                           int& dL, bool& x, int& rem, bool& finite) {
+  const int st = (E > S) - (E < S);
+  rem = abs(E - S);
   const int room = st > 0 ? (n - 1 - S) : S;  // in-grid steps available
   f = (float)st;
-  e = (float)(S + (st > 0 ? 1 : 0));
-  inv = 0.0f;
-  key = 0.0f;
+  // no steps on this axis: key (e - s) * inv = (S + 1 - s) * +inf = +inf
+  e = (float)(S + (st >= 0 ? 1 : 0));
+  inv = __int_as_float(0x7f800000);
+  key = __int_as_float(0x7f800000);
+  x = rem > room;
+  c = x ? room : rem;
   if (rem > 0) {
     inv = __frcp_rn(__fsub_rn(g, s));
     key = __fmul_rn(__fsub_rn(e, s), inv);
+    finite = finite && isfinite(inv);
   }
-  c = rem <= room ? rem : room + 1;
-  if (rem > room) exitm |= bit;
   dL = st * stride;
 }
 
@@ -89,12 +124,14 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
   const int64_t p = point_index(tid, rings);
   const int lane = threadIdx.x & 31;
   const float s0 = sp.b[0], s1 = sp.b[1], s2 = sp.b[2];
+  const float kInf = __int_as_float(0x7f800000);
 
   bool active = false;
   float e0 = 0.f, e1 = 0.f, e2 = 0.f, f0 = 0.f, f1 = 0.f, f2 = 0.f;
-  float i0 = 0.f, i1 = 0.f, i2 = 0.f, k0 = 0.f, k1 = 0.f, k2 = 0.f;
-  int c0 = 0, c1 = 0, c2 = 0, dL0 = 0, dL1 = 0, dL2 = 0;
-  uint32_t exitm = 0, L = 0;
+  float i0 = 0.f, i1 = 0.f, i2 = 0.f, k0 = kInf, k1 = kInf, k2 = kInf;
+  int c0 = 0, c1 = 0, c2 = 0, dL0 = 0, dL1 = 0, dL2 = 0, left = 0;
+  bool x0 = false, x1 = false, x2 = false;
+  uint32_t L = 0;
 
   if (p < n) {
     const float4 q = __ldg(pts + p);
@@ -108,15 +145,26 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
         const uint32_t LE = (uint32_t)(E2 + d.nz * E0 + strideY * E1);
         atomicOr(bits + (LE >> 5), 1u << (LE & 31));
       }
-      axis_setup(sp.S[0], E0, g0, s0, d.nx, d.nz, 1, e0, f0, i0, k0, c0, dL0, exitm);
-      axis_setup(sp.S[1], E1, g1, s1, d.ny, strideY, 2, e1, f1, i1, k1, c1, dL1, exitm);
-      axis_setup(sp.S[2], E2, g2, s2, d.nz, 1, 4, e2, f2, i2, k2, c2, dL2, exitm);
+      int r0, r1, r2;
+      bool fin = true;
+      axis_setup(sp.S[0], E0, g0, s0, d.nx, d.nz, e0, f0, i0, k0, c0, dL0, x0, r0, fin);
+      axis_setup(sp.S[1], E1, g1, s1, d.ny, strideY, e1, f1, i1, k1, c1, dL1, x1, r1, fin);
+      axis_setup(sp.S[2], E2, g2, s2, d.nz, 1, e2, f2, i2, k2, c2, dL2, x2, r2, fin);
       L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]);
-      active = (c0 | c1 | c2) != 0;  // the sensor voxel is in the grid (host check)
+      // steps until E when no axis exits the grid; otherwise the exit ends it
+      // (a walk never takes more than nx+ny+nz in-grid steps: hard cap)
+      left = (x0 || x1 || x2) ? d.nx + d.ny + d.nz : r0 + r1 + r2;
+      active = (r0 | r1 | r2) != 0;  // the sensor voxel is in the grid (host check)
+      if (active && !fin) {
+        const int S[3] = {sp.S[0], sp.S[1], sp.S[2]}, E[3] = {E0, E1, E2};
+        const float g[3] = {g0, g1, g2}, s[3] = {s0, s1, s2};
+        walk_exact(S, E, g, s, d, miss);
+        active = false;
+      }
     }
   }
 
-  const bool x0 = exitm & 1u, x1 = exitm & 2u, x2 = exitm & 4u;
+  const unsigned after = 0xfffffffeu << lane;  // lanes above this one
   unsigned act = __ballot_sync(0xffffffffu, active);
   while (act) {
     // Merge equal voxels of adjacent lanes: one atomic per run of lanes.
@@ -124,35 +172,41 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
     const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
     const bool head = active && (lane == 0 || prev != key);
     const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const unsigned boundary = (heads | ~act) & (0xfffffffeu << lane);  // lanes > lane
-    const uint32_t cnt = (uint32_t)(__clz(__brev(boundary)) - lane);   // run length
+    const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after)) - lane);
     asm volatile(
         "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
         "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
         "r"(cnt), "r"((uint32_t)head)
         : "memory");
-    // One DDA step for every lane (inactive lanes compute garbage that is
-    // never emitted: `active` only ever goes from true to false).
-    // argmin over axes with steps left, ties to the lowest axis (O5)
-    const bool p0 = c0 > 0, p1 = c1 > 0, p2 = c2 > 0;
-    const bool use1 = p1 && (!p0 || k1 < k0);
-    const float bk = use1 ? k1 : k0;
-    const bool use2 = p2 && (!(p0 || use1) || k2 < bk);
-    const bool a1 = use1 && !use2;
-    const bool a0 = !use1 && !use2;
-    e0 = a0 ? __fadd_rn(e0, f0) : e0;
-    e1 = a1 ? __fadd_rn(e1, f1) : e1;
-    e2 = use2 ? __fadd_rn(e2, f2) : e2;
-    c0 -= a0;
-    c1 -= a1;
-    c2 -= use2;
-    L += (uint32_t)(use2 ? dL2 : (a1 ? dL1 : dL0));
+    // One DDA step for every lane; inactive lanes compute values that are
+    // never emitted (`active` only goes from true to false).
+    const bool l10 = k1 < k0;
+    const float b01 = l10 ? k1 : k0;
+    const bool u2 = k2 < b01;
+    const bool u1 = l10 && !u2;
+    const bool u0 = !l10 && !u2;
+    const int cs = u2 ? c2 : (u1 ? c1 : c0);
+    const bool xs = u2 ? x2 : (u1 ? x1 : x0);
+    const bool out = xs && cs == 0;  // this step would leave the grid
+    e0 = u0 ? __fadd_rn(e0, f0) : e0;
+    e1 = u1 ? __fadd_rn(e1, f1) : e1;
+    e2 = u2 ? __fadd_rn(e2, f2) : e2;
+    c0 -= u0;
+    c1 -= u1;
+    c2 -= u2;
+    L += (uint32_t)(u2 ? dL2 : (u1 ? dL1 : dL0));
+    // A non-exit axis that used its last step gets 1/d = +-inf: its key
+    // (e - s) * inv is then +inf for good (e - s is nonzero with the sign of
+    // the step once the axis has moved).
+    const bool exh = !xs && cs == 1;
+    i0 = (u0 && exh) ? f0 * kInf : i0;
+    i1 = (u1 && exh) ? f1 * kInf : i1;
+    i2 = (u2 && exh) ? f2 * kInf : i2;
     k0 = __fmul_rn(__fsub_rn(e0, s0), i0);
     k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
     k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
-    // an exit axis reaching 0 means the step left the grid
-    const bool out = (x0 && c0 == 0) || (x1 && c1 == 0) || (x2 && c2 == 0);
-    active = active && !out && (c0 | c1 | c2) != 0;
+    --left;
+    active = active && !out && left != 0;
     act = __ballot_sync(0xffffffffu, active);
   }
 }
@@ -317,6 +371,114 @@ __global__ void __launch_bounds__(256) k_finalize(int32_t* __restrict__ buf,
   }
 }
 
+// Single-pass rank of the occupied voxels (decoupled look-back scan over the
+// occupancy bitmask): absolute exclusive popcount prefix per 32-voxel word, so
+// rank(L) = wprefix[L>>5] + popc(bits[L>>5] & ((1<<(L&31))-1)) is the voxel's
+// index in L order (reading A2, deterministic).  Tiles are taken in launch
+// order from a ticket counter; status words carry an epoch so nothing needs
+// resetting between calls.
+constexpr uint64_t kFlagIncl = 1ull << 32;
+
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  return cuda::atomic_ref<const uint64_t, cuda::thread_scope_device>(*p).load(
+      cuda::memory_order_acquire);
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  cuda::atomic_ref<uint64_t, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_release);
+}
+
+__global__ void __launch_bounds__(kRankThreads) k_rank(const uint32_t* __restrict__ bits,
+                                                       int64_t W, uint32_t* __restrict__ wprefix,
+                                                       uint64_t* __restrict__ status,
+                                                       unsigned long long* __restrict__ ticket,
+                                                       uint64_t base, uint32_t epoch,
+                                                       int64_t nblk,
+                                                       uint32_t* __restrict__ total_out) {
+  __shared__ uint32_t wsum[kRankThreads / 32];
+  __shared__ uint32_t sprefix;
+  __shared__ int64_t sbid;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  if (t == 0) sbid = (int64_t)(atomicAdd(ticket, 1ull) - base);
+  __syncthreads();
+  const int64_t bid = sbid;
+  const int64_t w0 = bid * kRankWordsPerBlock + t * 4;
+  uint32_t w4[4];
+  if (w0 + 3 < W) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(bits + w0));
+    w4[0] = v.x;
+    w4[1] = v.y;
+    w4[2] = v.z;
+    w4[3] = v.w;
+  } else {
+    for (int i = 0; i < 4; ++i) w4[i] = (w0 + i < W) ? bits[w0 + i] : 0u;
+  }
+  const uint32_t c0 = __popc(w4[0]), c1 = __popc(w4[1]), c2 = __popc(w4[2]), c3 = __popc(w4[3]);
+  const uint32_t tsum = c0 + c1 + c2 + c3;
+  const uint32_t inc = warp_incl_scan(tsum, lane);
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = lane < kRankThreads / 32 ? wsum[lane] : 0u;
+    const uint32_t i = warp_incl_scan(v, lane);
+    if (lane < kRankThreads / 32) wsum[lane] = i - v;  // exclusive per warp
+    const uint32_t total = __shfl_sync(0xffffffffu, i, kRankThreads / 32 - 1);
+    const uint64_t ep = (uint64_t)epoch << 33;
+    if (bid == 0) {
+      if (lane == 0) {
+        st_release(status, ep | kFlagIncl | total);
+        sprefix = 0;
+      }
+    } else {
+      if (lane == 0) st_release(status + bid, ep | total);
+      // look back over predecessors, 32 at a time
+      uint32_t prefix = 0;
+      int64_t jb = bid - 1;
+      for (;;) {
+        const int64_t j = jb - lane;
+        uint64_t sv = j >= 0 ? ld_acquire(status + j) : (ep | kFlagIncl);
+        while (__any_sync(0xffffffffu, (sv >> 33) != epoch)) {
+          if ((sv >> 33) != epoch) sv = ld_acquire(status + j);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, (sv & kFlagIncl) != 0);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+        uint32_t val = lane <= stop ? (uint32_t)sv : 0u;
+        val = __reduce_add_sync(0xffffffffu, val);
+        prefix += val;
+        if (incl) break;
+        jb -= 32;
+      }
+      if (lane == 0) {
+        st_release(status + bid, ep | kFlagIncl | (prefix + total));
+        sprefix = prefix;
+      }
+    }
+    if (lane == 0 && bid == nblk - 1) *total_out = (bid == 0 ? 0u : sprefix) + total;
+  }
+  __syncthreads();
+  const uint32_t p0 = sprefix + wsum[wid] + inc - tsum;
+  if (w0 + 3 < W) {
+    *reinterpret_cast<uint4*>(wprefix + w0) = make_uint4(p0, p0 + c0, p0 + c0 + c1,
+                                                         p0 + c0 + c1 + c2);
+  } else {
+    const uint32_t pp[4] = {p0, p0 + c0, p0 + c0 + c1, p0 + c0 + c1 + c2};
+    for (int i = 0; i < 4; ++i)
+      if (w0 + i < W) wprefix[w0 + i] = pp[i];
+  }
+}
+
+// Zero two regions in one launch (the slot's LUT-as-miss-grid and bitmask).
+__global__ void __launch_bounds__(256) k_zero2(uint4* __restrict__ a, int64_t na16,
+                                               uint4* __restrict__ b, int64_t nb16) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na16 + nb16; i += stride) {
+    if (i < na16)
+      __stcs(a + i, z);
+    else
+      __stcs(b + (i - na16), z);
+  }
+}
+
 // per-word absolute prefix only (merged-map export)
 __global__ void __launch_bounds__(kRankThreads) k_prefix_only(const uint32_t* __restrict__ bits,
                                                               uint32_t* __restrict__ wprefix,
@@ -392,6 +554,25 @@ cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const ui
   const int64_t threads = (d.V + 3) / 4;
   k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(lut_inplace, bits, wprefix, data,
                                                                 d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
+                        unsigned long long* ticket, uint64_t base, uint32_t epoch,
+                        uint32_t* total, cudaStream_t st) {
+  const int64_t nblk = rank_blocks(d);
+  k_rank<<<(unsigned)nblk, kRankThreads, 0, st>>>(bits, d.W, wprefix, status, ticket, base, epoch,
+                                                   nblk, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero2(void* a, size_t abytes, void* b, size_t bbytes, cudaStream_t st) {
+  const int64_t n = (int64_t)(abytes / 16 + bbytes / 16);
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_zero2<<<(unsigned)blocks, 256, 0, st>>>((uint4*)a, (int64_t)(abytes / 16), (uint4*)b,
+                                            (int64_t)(bbytes / 16));
   return cudaGetLastError();
 }
 

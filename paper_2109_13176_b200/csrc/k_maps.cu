@@ -42,35 +42,6 @@ __device__ __forceinline__ bool slot_rank(const SlotView& s, int64_t L, uint32_t
   return true;
 }
 
-struct Merged {
-  uint64_t H, Mi;
-  uint32_t mn;
-};
-
-// O7 for one output voxel (x, y, z): sum hits/misses, min of min_dz.
-__device__ __forceinline__ Merged merge_voxel(const SlotSet& ss, const Dims& d, int x, int y,
-                                              int z) {
-  Merged m{0, 0, 0xffffffffu};
-  for (int k = 0; k < ss.K; ++k) {
-    const SlotView& s = ss.s[k];
-    const int ux = x + s.dx, uy = y + s.dy, uz = z + s.dz;
-    if ((unsigned)ux >= (unsigned)d.nx || (unsigned)uy >= (unsigned)d.ny ||
-        (unsigned)uz >= (unsigned)d.nz)
-      continue;
-    const int64_t L = (int64_t)uz + (int64_t)d.nz * ((int64_t)ux + (int64_t)d.nx * uy);
-    uint32_t r;
-    if (slot_rank(s, L, r)) {
-      const uint4 row = __ldg(reinterpret_cast<const uint4*>(s.data + r));
-      m.H += row.x;
-      m.Mi += row.y;
-      m.mn = min(m.mn, row.z);
-    } else {
-      m.Mi += (uint64_t)(-1ll - (int64_t)__ldg(s.lut + L));
-    }
-  }
-  return m;
-}
-
 // Segmented (within groups of 2^lg lanes) reductions.
 __device__ __forceinline__ uint32_t grp_or(uint32_t v, int lg) {
   for (int o = 1; o < (1 << lg); o <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
@@ -339,21 +310,23 @@ __device__ __forceinline__ bool ring_line(const uint32_t* __restrict__ bm, int l
   return found;
 }
 
-// O10: negative obstacles for undefined cells.  Ring k of cone +x is
-// the column segment x+k, y-k..y+k: tested 32 cells per bitmask word.
+// O10: negative obstacles for undefined cells.  A block is 32
+// consecutive cells x 4 cones: warp w searches cone w for its 32 cells (lanes
+// of a warp probe neighbouring rings, so they run similar distances); the
+// four cones are combined through shared memory.  Ring k of cone +x is the
+// column segment (x+k, y-k..y+k), tested 32 cells per bitmask word.
 __global__ void __launch_bounds__(128) k_negative(const Dims d, const LayerParams lp,
                                                   const LayerPtrs out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)d.nx * d.ny) return;
-  const int x = (int)(c % d.nx), y = (int)(c / d.nx);
+  __shared__ int32_t smin[4][32], smax[4][32], scnt[4][32];
+  const int tx = threadIdx.x, cone = threadIdx.y;
+  const int64_t cells = (int64_t)d.nx * d.ny;
+  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
   const int32_t* __restrict__ qs = out.qs;
-  if (__ldg(qs + c) != kQsUndef) {
-    out.neg[c] = 0;
-    return;
-  }
-  const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
+  const bool undef = c < cells && __ldg(qs + c) == kQsUndef;
   int64_t fmin = INT64_MAX, fmax = INT64_MIN, fcount = 0;
-  for (int cone = 0; cone < 4; ++cone) {
+  if (undef) {
+    const int x = (int)(c % d.nx), y = (int)(c / d.nx);
+    const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
     const bool alongx = cone < 2;  // +x / -x cones: ring lines are columns
     const int sgn = (cone & 1) ? -1 : 1;
     const int base = alongx ? x : y;
@@ -374,7 +347,20 @@ __global__ void __launch_bounds__(128) k_negative(const Dims d, const LayerParam
       if (found) break;
     }
   }
-  out.neg[c] = (fcount >= 2 && (fmax - fmin) > lp.T_neg) ? 1 : 0;
+  smin[cone][tx] = fcount ? (int32_t)fmin : INT32_MAX;
+  smax[cone][tx] = fcount ? (int32_t)fmax : INT32_MIN;
+  scnt[cone][tx] = (int32_t)fcount;
+  __syncthreads();
+  if (cone == 0 && c < cells) {
+    int32_t mn = smin[0][tx], mx = smax[0][tx], n = scnt[0][tx];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+      mn = min(mn, smin[j][tx]);
+      mx = max(mx, smax[j][tx]);
+      n += scnt[j][tx];
+    }
+    out.neg[c] = (undef && n >= 2 && (int64_t)mx - (int64_t)mn > lp.T_neg) ? 1 : 0;
+  }
 }
 
 // merged occupancy bits of the combined map (export path)
@@ -454,6 +440,21 @@ __global__ void __launch_bounds__(256) k_merge_write(const SlotSet ss, const Dim
   }
 }
 
+// All 2D layers in one launch: blockIdx.y selects the layer; 16-byte chunks.
+__global__ void __launch_bounds__(256) k_export_layers(const __grid_constant__ CopyJob job) {
+  const int l = blockIdx.y;
+  const int64_t n16 = job.bytes[l] >> 4;
+  const uint4* __restrict__ src = reinterpret_cast<const uint4*>(job.src[l]);
+  uint4* __restrict__ dst = reinterpret_cast<uint4*>(job.dst[l]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcs(src + i);
+  if (blockIdx.x == 0 && threadIdx.x < (job.bytes[l] & 15)) {
+    const int64_t b = (n16 << 4) + threadIdx.x;
+    reinterpret_cast<uint8_t*>(job.dst[l])[b] = reinterpret_cast<const uint8_t*>(job.src[l])[b];
+  }
+}
+
 inline unsigned cells_blocks(const Dims& d, int tpb) {
   return (unsigned)(((int64_t)d.nx * d.ny + tpb - 1) / tpb);
 }
@@ -475,7 +476,17 @@ cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& 
 
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                             cudaStream_t st) {
-  k_negative<<<cells_blocks(d, 128), 128, 0, st>>>(d, lp, out);
+  k_negative<<<cells_blocks(d, 32), dim3(32, 4), 0, st>>>(d, lp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st) {
+  int64_t mx = 0;
+  for (int l = 0; l < GVOM_LAYER_COUNT; ++l) mx = job.bytes[l] > mx ? job.bytes[l] : mx;
+  int64_t blocks = ((mx >> 4) + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  k_export_layers<<<dim3((unsigned)blocks, GVOM_LAYER_COUNT), 256, 0, st>>>(job);
   return cudaGetLastError();
 }
 

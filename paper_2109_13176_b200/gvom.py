@@ -88,6 +88,7 @@ def load_library() -> C.CDLL:
         "gvom_integrate_scan": ([P, P, I32], I32),
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
+        "gvom_export_layers": ([P, P, P], I32),
         "gvom_map_origin": ([P, P], I32),
         "gvom_export_voxels": ([P, P, P, I64, P], I32),
         "gvom_export_frame": ([P, I32, P, P, I64, P, P], I32),
@@ -107,7 +108,7 @@ def load_library() -> C.CDLL:
 
 EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_stream",
             "gvom_synchronize", "gvom_shift", "gvom_integrate_scan", "gvom_compute_maps",
-            "gvom_export_2d", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
+            "gvom_export_2d", "gvom_export_layers", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version")
 
@@ -236,9 +237,19 @@ class GvomMap:
         return out
 
     def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None) -> Dict[str, torch.Tensor]:
+        """All seven layers with one gvom_export_layers call (one kernel when
+        every destination is device memory)."""
         res = {}
         for name in LAYERS:
-            res[name] = self.export_2d(name, None if out is None else out[name])
+            t = None if out is None else out[name]
+            if t is None:
+                dt = torch.uint8 if name in LAYER_U8 else torch.float32
+                t = torch.empty((self.ny, self.nx), dtype=dt, device=self.device)
+            assert t.is_contiguous()
+            res[name] = t
+        ptrs = (C.c_void_p * 7)(*[res[n].data_ptr() for n in LAYERS])
+        sizes = (C.c_size_t * 7)(*[res[n].numel() * res[n].element_size() for n in LAYERS])
+        _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
         return res
 
     def map_origin(self) -> np.ndarray:
