@@ -89,9 +89,9 @@ Layout make_layout(const gvom_config* c) {
   off += 3 * align_up((size_t)l.cells);
   l.qs = off;
   off += align_up(4 * (size_t)l.cells);
-  l.defbits = off;  // row + column defined-surface bitmasks
-  l.defbits_bytes = 4 * ((size_t)c->ny * ((c->nx + 31) / 32) + (size_t)c->nx * ((c->ny + 31) / 32));
-  off += align_up(l.defbits_bytes);
+  l.defbits = off;  // qsT, nmin, nmax for the negative-obstacle cone sweeps
+  l.defbits_bytes = 3 * align_up(4 * (size_t)l.cells);
+  off += l.defbits_bytes;
   l.mbits = off;
   off += align_up(4 * (size_t)d.W);
   l.mprefix = off;
@@ -310,8 +310,9 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
   h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
   h->layers.qs = (int32_t*)(h->ws + lay.qs);
-  h->layers.rowbits = (uint32_t*)(h->ws + lay.defbits);
-  h->layers.colbits = h->layers.rowbits + (size_t)cfg->ny * ((cfg->nx + 31) / 32);
+  h->layers.qsT = (int32_t*)(h->ws + lay.defbits);
+  h->layers.nmin = (int32_t*)(h->ws + lay.defbits + align_up(4 * (size_t)lay.cells));
+  h->layers.nmax = (int32_t*)(h->ws + lay.defbits + 2 * align_up(4 * (size_t)lay.cells));
   h->mbits = (uint32_t*)(h->ws + lay.mbits);
   h->mprefix = (uint32_t*)(h->ws + lay.mprefix);
   // integer thresholds
@@ -447,16 +448,13 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
   h->map_slots = buffer_slots(h, o);
   h->lp.o_z = o[2];
-  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
-    return cudaMemsetAsync(h->layers.rowbits, 0, h->lay.defbits_bytes, h->st);
-  }));
   GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
     return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st);
   }));
-  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
-                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
   GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
                 [&] { return launch_negative(h->d, h->lp, h->layers, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
+                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
   for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
   h->maps_valid = true;
   return GVOM_OK;

@@ -51,9 +51,10 @@ struct LayerPtrs {
   uint8_t* neg;
   float* slope;
   float* rough;
-  int32_t* qs;
-  uint32_t* rowbits;  // [ny][ceil(nx/32)] defined-surface bits along x
-  uint32_t* colbits;  // [nx][ceil(ny/32)] defined-surface bits along y
+  int32_t* qs;    // [ny][nx] fixed-point surface q_s, kQsUndef if undefined
+  int32_t* qsT;   // [nx][ny] transposed copy (cone sweeps along x read it by line)
+  int32_t* nmin;  // [ny][nx] min / max of the heights found by the cone search
+  int32_t* nmax;
 };
 
 struct LayerParams {
@@ -86,7 +87,7 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st);
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
-                            cudaStream_t st);
+                            cudaStream_t st);  // cone sweeps -> nmin / nmax (slope writes neg)
 cudaError_t launch_merge_bits(const SlotSet& ss, const Dims& d, uint32_t* mbits, cudaStream_t st);
 cudaError_t launch_merge_write(const SlotSet& ss, const Dims& d, const uint32_t* mbits,
                                const uint32_t* mprefix, int32_t* lut, gvom_voxel* data,

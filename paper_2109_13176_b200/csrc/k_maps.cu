@@ -56,29 +56,56 @@ __device__ __forceinline__ uint32_t grp_min(uint32_t v, int lg) {
   return v;
 }
 
-// O7 + O8 fused, one warp per output column.  Lane (g, k): slot k = lane mod
-// 2^lg of group g = lane >> lg.  Groups scan different 32-z chunks, then
-// evaluate different candidate voxels of the column in parallel; each voxel is
-// the sum / min over the slots of its group (segmented shuffles).
+// One slot's contribution to output voxel z of this lane's column (O7):
+// hits, misses (data row if occupied, -1 - LUT if empty), min_dz.
+struct SlotVox {
+  uint32_t h, mi, mn;
+};
+__device__ __forceinline__ SlotVox slot_vox(bool col, const int32_t* __restrict__ lut,
+                                            const gvom_voxel* __restrict__ data, int64_t cb,
+                                            int uz, int nz) {
+  SlotVox r{0u, 0u, 0xffffffffu};
+  if (col && (unsigned)uz < (unsigned)nz) {
+    const int32_t v = __ldg(lut + cb + uz);
+    if (v >= 0) {
+      const uint4 row = __ldg(reinterpret_cast<const uint4*>(data + v));
+      r.h = row.x;
+      r.mi = row.y;
+      r.mn = row.z;
+    } else {
+      r.mi = (uint32_t)(-1 - v);
+    }
+  }
+  return r;
+}
+
+// O7 + O8 fused.  2^lg lanes per output column, lane k <-> buffer map k
+// (32 >> lg columns per warp).  Per column:
+//   z*   : lowest z occupied in any map (OR of the maps' shifted occupancy
+//          bits), mn(z*) = min over maps -> q_s.
+//   band : voxels strictly between z_lo = (q_s+T_lo)>>16 and z_hi =
+//          (q_s+T_hi)>>16 are in [T_lo, T_hi] whatever their min_dz, so each
+//          lane sums its own map's hits / hits+misses over them with no
+//          cross-lane traffic; only the two edge voxels need the merged
+//          min_dz (a group min).  One group sum at the end.
 __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
                                                  const LayerParams lp, const LayerPtrs out) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= (int64_t)d.nx * d.ny) return;  // warp-uniform
-  const int x = (int)(c % d.nx), y = (int)(c / d.nx);
   const int lg = ss.kp_log2;
   const int k = lane & ((1 << lg) - 1);
-  const int g = lane >> lg;
-  const int G = 32 >> lg;
-  // this lane's slot column
+  const int64_t cells = (int64_t)d.nx * d.ny;
+  const int64_t c0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - lg);
+  if (c0 >= cells) return;  // whole warp past the end
+  const int64_t c = c0 + (lane >> lg);
+  const bool cvalid = c < cells;
+  const int x = cvalid ? (int)(c % d.nx) : 0, y = cvalid ? (int)(c / d.nx) : 0;
   bool col = false;
   int64_t cb = 0;
   int dz = 0;
   const uint32_t* bits = nullptr;
-  const uint32_t* wpre = nullptr;
-  const gvom_voxel* data = nullptr;
   const int32_t* lut = nullptr;
-  if (k < ss.K) {
+  const gvom_voxel* data = nullptr;
+  if (cvalid && k < ss.K) {
     const SlotView& s = ss.s[k];
     const int sx = x + s.dx, sy = y + s.dy;
     if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny) {
@@ -86,126 +113,97 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
       cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
       dz = s.dz;
       bits = s.bits;
-      wpre = s.wprefix;
-      data = s.data;
       lut = s.lut;
+      data = s.data;
     }
   }
-  // ---- z*: lowest z occupied in any buffer map ----
-  int zs = -1;
-  for (int zb = 0; zb < d.nz && zs < 0; zb += 32 * G) {
-    const int z0 = zb + 32 * g;
-    uint32_t m = (col && z0 < d.nz) ? col_bits32(bits, d.W, cb, z0 + dz, d.nz) : 0u;
+  // ---- z*: merged occupancy, 32 z at a time; keep a 64-z window from the
+  // chunk holding z* ----
+  int zs = -1, zc = 0;
+  uint64_t occ = 0;
+  for (int z0 = 0; z0 < d.nz; z0 += 32) {
+    uint32_t m = col ? col_bits32(bits, d.W, cb, z0 + dz, d.nz) : 0u;
     m = grp_or(m, lg);
-    const unsigned nzg = __ballot_sync(0xffffffffu, m != 0u && k == 0);
-    if (nzg) {
-      const int gl = __ffs(nzg) - 1;  // leader lane of the lowest non-empty chunk
-      const uint32_t mm = __shfl_sync(0xffffffffu, m, gl);
-      zs = zb + 32 * (gl >> lg) + __ffs(mm) - 1;
+    if (zs >= 0) {
+      if (z0 == zc + 32) occ |= (uint64_t)m << 32;  // the chunk after z*'s
+    } else if (m) {
+      zs = z0 + __ffs(m) - 1;
+      zc = z0;
+      occ = m;
+    }
+    if (__all_sync(0xffffffffu, zs >= 0 ? z0 >= zc + 32 : !cvalid)) break;
+  }
+  // ---- the surface voxel ----
+  const SlotVox v0 = slot_vox(col && zs >= 0, lut, data, cb, zs + dz, d.nz);
+  const uint32_t mn0 = grp_min(v0.mn, lg);
+  const int64_t q_s = 65536ll * zs + (int64_t)mn0;
+  const int z_lo = (int)((q_s + lp.T_lo) >> 16);
+  const int64_t zh = (q_s + lp.T_hi) >> 16;
+  const int z_hi = (int)(zh < (int64_t)d.nz - 1 ? zh : (int64_t)d.nz - 1);
+  uint64_t SH = 0, SW = 0;
+  if (zs >= 0) {
+    // interior band voxels: certainly in the band when occupied
+    for (int z = z_lo + 1; z < z_hi; ++z) {
+      const int rel = z - zc;
+      bool occz;
+      if (rel < 64) {
+        occz = (occ >> rel) & 1ull;
+      } else {  // band wider than the 64-z window (not in the shipped configs)
+        occz = false;
+        for (int kk = 0; kk < ss.K; ++kk) {
+          const SlotView& s = ss.s[kk];
+          const int sx = x + s.dx, sy = y + s.dy, uz = z + s.dz;
+          if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny &&
+              (unsigned)uz < (unsigned)d.nz &&
+              __ldg(s.lut + (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy) + uz) >= 0)
+            occz = true;
+        }
+      }
+      if (!occz) continue;
+      const SlotVox v = slot_vox(col, lut, data, cb, z + dz, d.nz);
+      SH += v.h;
+      SW += (uint64_t)v.h + v.mi;
     }
   }
-  if (zs < 0) {
-    if (lane == 0) {
-      out.hard[c] = 0;
-      out.soft[c] = 0;
-      out.height[c] = __int_as_float(0x7fc00000);
-      out.density[c] = __int_as_float(0x7fc00000);
-      out.qs[c] = kQsUndef;
+  // edge voxels z_lo and z_hi need the merged min_dz (uniform code)
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int z = e == 0 ? z_lo : z_hi;
+    const bool use = zs >= 0 && z <= z_hi && z >= zs && (e == 0 || z_hi != z_lo);
+    const SlotVox v = use ? slot_vox(col, lut, data, cb, z + dz, d.nz) : SlotVox{0u, 0u, 0xffffffffu};
+    const uint32_t mn = grp_min(v.mn, lg);
+    if (use && mn != 0xffffffffu) {
+      const int64_t dq = (65536ll * z + (int64_t)mn) - q_s;
+      if (dq >= lp.T_lo && dq <= lp.T_hi) {
+        SH += v.h;
+        SW += (uint64_t)v.h + v.mi;
+      }
     }
+  }
+  SH = grp_add64(SH, lg);
+  SW = grp_add64(SW, lg);
+  if (k != 0 || !cvalid) return;
+  out.hard[c] = 0;
+  out.soft[c] = 0;
+  out.nmin[c] = INT32_MAX;
+  out.nmax[c] = INT32_MIN;
+  const int32_t qv = zs < 0 ? kQsUndef : (int32_t)q_s;
+  out.qs[c] = qv;
+  out.qsT[(int64_t)x * d.ny + y] = qv;
+  if (zs < 0) {
+    out.height[c] = __int_as_float(0x7fc00000);
+    out.density[c] = __int_as_float(0x7fc00000);
     return;
   }
-  // ---- candidates: merged occupancy in a window starting at z* ----
-  const int span = (int)((lp.T_hi >> 16) + 1);  // band top is at most z* + span
-  int64_t q_s = 0;
-  int zhi = zs;
-  uint64_t SH = 0, SW = 0;
-  bool have_qs = false;
-  for (int w0 = zs; w0 <= zs + span && w0 < d.nz; w0 += 32) {
-    uint32_t wm = col ? col_bits32(bits, d.W, cb, w0 + dz, d.nz) : 0u;
-    wm = grp_or(wm, lg);  // identical in every group
-    if (have_qs) {
-      const int lim = zhi - w0;  // keep z <= zhi
-      if (lim < 0) break;
-      if (lim < 31) wm &= (2u << lim) - 1u;
-    }
-    while (wm) {
-      // group g takes the g-th remaining candidate of this batch
-      uint32_t t = wm;
-      for (int i = 0; i < g && t; ++i) t &= t - 1;
-      const bool has = t != 0u;
-      const int z = has ? w0 + __ffs(t) - 1 : -1;
-      // remove G candidates from wm
-      for (int i = 0; i < G && wm; ++i) wm &= wm - 1;
-      uint32_t h = 0, mi = 0, mn = 0xffffffffu;
-      if (has && col) {
-        const int uz = z + dz;
-        if ((unsigned)uz < (unsigned)d.nz) {
-          const int64_t L = cb + uz;
-          const int64_t wi = L >> 5;
-          const int bit = (int)(L & 31);
-          const uint32_t bw = __ldg(bits + wi);
-          if ((bw >> bit) & 1u) {
-            const uint32_t r = __ldg(wpre + wi) + __popc(bw & ((1u << bit) - 1u));
-            const uint4 row = __ldg(reinterpret_cast<const uint4*>(data + r));
-            h = row.x;
-            mi = row.y;
-            mn = row.z;
-          } else {
-            mi = (uint32_t)(-1 - __ldg(lut + L));
-          }
-        }
-      }
-      const uint64_t H = grp_add64(h, lg);
-      const uint64_t Mi = grp_add64(mi, lg);
-      const uint32_t MN = grp_min(mn, lg);
-      if (!have_qs) {
-        // the first candidate of the first batch (group 0) is z* itself
-        const uint32_t mn0 = __shfl_sync(0xffffffffu, MN, 0);
-        q_s = 65536ll * zs + (int64_t)mn0;
-        const int64_t zh = (lp.T_hi + q_s) >> 16;
-        zhi = (int)(zh < (int64_t)d.nz - 1 ? zh : (int64_t)d.nz - 1);
-        have_qs = true;
-      }
-      if (k == 0 && has && z <= zhi) {
-        const int64_t dq = (65536ll * z + (int64_t)MN) - q_s;
-        if (dq >= lp.T_lo && dq <= lp.T_hi) {
-          SH += H;
-          SW += H + Mi;
-        }
-      }
-      // drop candidates above zhi (uniform: zhi and wm are warp-uniform)
-      const int lim = zhi - w0;
-      if (lim < 0)
-        wm = 0u;
-      else if (lim < 31)
-        wm &= (2u << lim) - 1u;
-    }
-    // (uniform) stop once past zhi
-    if (w0 + 32 > zhi) break;
-  }
-  // sum the group leaders' partial band sums (non-leaders hold 0)
-  for (int o = 16; o > 0; o >>= 1) {
-    SH += __shfl_xor_sync(0xffffffffu, SH, o);
-    SW += __shfl_xor_sync(0xffffffffu, SW, o);
-  }
-  if (lane == 0) {
-    out.qs[c] = (int32_t)q_s;
-    out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
-    uint8_t hard = 0, soft = 0;
-    if (SH == 0) {
-      out.density[c] = 0.0f;
-    } else {
-      out.density[c] = (float)((double)SH / (double)SW);
-      if (65536ull * SH >= (uint64_t)lp.tau * SW)
-        hard = 1;
-      else
-        soft = 1;
-    }
-    out.hard[c] = hard;
-    out.soft[c] = soft;
-    const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
-    atomicOr(out.rowbits + (int64_t)y * WX + (x >> 5), 1u << (x & 31));
-    atomicOr(out.colbits + (int64_t)x * WY + (y >> 5), 1u << (y & 31));
+  out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
+  if (SH == 0) {
+    out.density[c] = 0.0f;
+  } else {
+    out.density[c] = (float)((double)SH / (double)SW);
+    if (65536ull * SH >= (uint64_t)lp.tau * SW)
+      out.hard[c] = 1;
+    else
+      out.soft[c] = 1;
   }
 }
 
@@ -214,29 +212,47 @@ __device__ __forceinline__ int64_t det3(int64_t a, int64_t b, int64_t c, int64_t
   return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
 }
 
-// O9: plane fit over the defined in-map cells of the N x N window
-__global__ void __launch_bounds__(128) k_slope(const Dims d, const LayerParams lp,
-                                               const LayerPtrs out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)d.nx * d.ny) return;
-  const int x = (int)(c % d.nx), y = (int)(c / d.nx);
-  const float qnan = __int_as_float(0x7fc00000);
+// O9: plane fit over the defined in-map cells of the N x N window.
+// A 32 x 8 tile of cells plus an r-cell halo of q_s is staged in shared
+// memory (kQsUndef = undefined or outside the map), then each thread builds
+// the exact int64 normal equations of its window.
+constexpr int kSlopeTX = 32, kSlopeTY = 8, kSlopeHalo = 4;  // r <= 4 (N <= 9)
+__global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, const LayerParams lp,
+                                                              const LayerPtrs out) {
+  constexpr int SW_ = kSlopeTX + 2 * kSlopeHalo, SH_ = kSlopeTY + 2 * kSlopeHalo;
+  __shared__ int32_t tile[SH_][SW_ + 1];
+  const int r = (lp.slope_window - 1) / 2;
+  const int x0 = blockIdx.x * kSlopeTX, y0 = blockIdx.y * kSlopeTY;
   const int32_t* __restrict__ qs = out.qs;
-  const int32_t qc = __ldg(qs + c);
+  for (int i = threadIdx.y * kSlopeTX + threadIdx.x; i < SW_ * SH_; i += kSlopeTX * kSlopeTY) {
+    const int ty = i / SW_, tx = i % SW_;
+    const int gx = x0 + tx - kSlopeHalo, gy = y0 + ty - kSlopeHalo;
+    tile[ty][tx] = ((unsigned)gx < (unsigned)d.nx && (unsigned)gy < (unsigned)d.ny)
+                       ? __ldg(qs + gx + (int64_t)d.nx * gy)
+                       : kQsUndef;
+  }
+  __syncthreads();
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x >= d.nx || y >= d.ny) return;
+  const int64_t c = x + (int64_t)d.nx * y;
+  const float qnan = __int_as_float(0x7fc00000);
+  const int cx = threadIdx.x + kSlopeHalo, cy = threadIdx.y + kSlopeHalo;
+  const int32_t qc = tile[cy][cx];
   if (qc == kQsUndef) {
+    // O10 decision for an undefined cell from the cone sweeps' min / max:
+    // max F - min F > T_neg (>= 0, so it implies |F| >= 2)
+    const int32_t mn = __ldg(out.nmin + c), mx = __ldg(out.nmax + c);
+    out.neg[c] = (mx != INT32_MIN && (int64_t)mx - (int64_t)mn > lp.T_neg) ? 1 : 0;
     out.slope[c] = qnan;
     out.rough[c] = qnan;
     return;
   }
-  const int r = (lp.slope_window - 1) / 2;
-  int64_t n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0, Sz = 0, Suz = 0, Svz = 0;
-  for (int v = -r; v <= r; ++v) {
-    const int yy = y + v;
-    if ((unsigned)yy >= (unsigned)d.ny) continue;
+  out.neg[c] = 0;
+  int32_t n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0;
+  int64_t Sz = 0, Suz = 0, Svz = 0;
+  for (int v = -r; v <= r; ++v)
     for (int u = -r; u <= r; ++u) {
-      const int xx = x + u;
-      if ((unsigned)xx >= (unsigned)d.nx) continue;
-      const int32_t q = __ldg(qs + xx + (int64_t)d.nx * yy);
+      const int32_t q = tile[cy + v][cx + u];
       if (q == kQsUndef) continue;
       const int64_t z = (int64_t)q - qc;
       n += 1;
@@ -249,7 +265,6 @@ __global__ void __launch_bounds__(128) k_slope(const Dims d, const LayerParams l
       Suz += u * z;
       Svz += v * z;
     }
-  }
   if (n < lp.min_plane_points) {
     out.slope[c] = qnan;
     out.rough[c] = qnan;
@@ -268,98 +283,190 @@ __global__ void __launch_bounds__(128) k_slope(const Dims d, const LayerParams l
   const double b = (double)Db / ((double)det * 65536.0);
   out.slope[c] = (float)atan(sqrt(a * a + b * b));
   double acc = 0.0;
-  for (int v = -r; v <= r; ++v) {
-    const int yy = y + v;
-    if ((unsigned)yy >= (unsigned)d.ny) continue;
+  for (int v = -r; v <= r; ++v)
     for (int u = -r; u <= r; ++u) {
-      const int xx = x + u;
-      if ((unsigned)xx >= (unsigned)d.nx) continue;
-      const int32_t q = __ldg(qs + xx + (int64_t)d.nx * yy);
+      const int32_t q = tile[cy + v][cx + u];
       if (q == kQsUndef) continue;
       const int64_t z = (int64_t)q - qc;
       const double e = (double)(det * z - Da * u - Db * v - Dc);
       acc += e * e;
     }
-  }
   const double sc = lp.res / 65536.0;
   out.rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
 }
 
-// Defined cells of one ring line (a row or column segment [lo, hi]) from the
-// defined-surface bitmask; for each, fold q into (min, max, count).
-__device__ __forceinline__ bool ring_line(const uint32_t* __restrict__ bm, int lo, int hi,
-                                          const int32_t* __restrict__ qs, int64_t q0,
-                                          int64_t qstride, int64_t& fmin, int64_t& fmax,
-                                          int64_t& fcount) {
-  bool found = false;
-  for (int wi = lo >> 5; wi <= (hi >> 5); ++wi) {
-    uint32_t w = __ldg(bm + wi);
-    const int b0 = wi << 5;
-    if (lo > b0) w &= ~0u << (lo - b0);
-    if (hi < b0 + 31) w &= (2u << (hi - b0)) - 1u;
-    while (w) {
-      const int i = b0 + __ffs(w) - 1;
-      w &= w - 1;
-      const int64_t q = __ldg(qs + q0 + qstride * i);
-      fmin = min(fmin, q);
-      fmax = max(fmax, q);
-      ++fcount;
-      found = true;
-    }
-  }
-  return found;
+// O10 cone search as a sweep.  For cone +x, let D(x,y) be the first ring k
+// (1..K) whose column segment {(x+k, y+t): |t| <= k} holds a defined cell,
+// and Mn / Mx the min / max q_s over the defined cells of that ring.  Ring k
+// of (x,y) is the union of ring k-1 of the sub-cones with apex (x+1, y-1),
+// (x+1, y), (x+1, y+1), so
+//   D(x,y) = 1                       if ring 1 (x+1, y-1..y+1) has a defined cell
+//          = 1 + min_t D(x+1, y+t)   otherwise (capped: > K = not found),
+// and Mn / Mx are the min / max over the sub-cones attaining that minimum
+// (their first rings are exactly the pieces of ring D of (x,y)).  The other
+// cones are the same sweep mirrored / transposed.  Apexes outside the map in
+// the cross direction (up to K cells) take part, since their cones reach in.
+// A block sweeps a tile of T lines plus a K-line halo (D <= K depends on at
+// most K lines ahead); every found (Mn, Mx) is folded into the cell's
+// nmin / nmax with atomics, and k_slope applies "max - min > T_neg".
+// Lines are streamed into a shared-memory ring by 1D TMA bulk copies
+// (cp.async.bulk, mbarrier completion) kNegRing lines ahead of the sweep.
+constexpr int kNegThreads = 512;
+constexpr int kNegRing = 8;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{ .reg .pred P1;\n"
+      "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=; }" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+// one elected thread: expect `bytes` on `bar`, then bulk-copy global -> shared
+__device__ __forceinline__ void tma_line(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t dsm = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dsm),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
 }
 
-// O10: negative obstacles for undefined cells.  A block is 32
-// consecutive cells x 4 cones: warp w searches cone w for its 32 cells (lanes
-// of a warp probe neighbouring rings, so they run similar distances); the
-// four cones are combined through shared memory.  Ring k of cone +x is the
-// column segment (x+k, y-k..y+k), tested 32 cells per bitmask word.
-__global__ void __launch_bounds__(128) k_negative(const Dims d, const LayerParams lp,
-                                                  const LayerPtrs out) {
-  __shared__ int32_t smin[4][32], smax[4][32], scnt[4][32];
-  const int tx = threadIdx.x, cone = threadIdx.y;
-  const int64_t cells = (int64_t)d.nx * d.ny;
-  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
-  const int32_t* __restrict__ qs = out.qs;
-  const bool undef = c < cells && __ldg(qs + c) == kQsUndef;
-  int64_t fmin = INT64_MAX, fmax = INT64_MIN, fcount = 0;
-  if (undef) {
-    const int x = (int)(c % d.nx), y = (int)(c / d.nx);
-    const int WX = (d.nx + 31) >> 5, WY = (d.ny + 31) >> 5;
-    const bool alongx = cone < 2;  // +x / -x cones: ring lines are columns
-    const int sgn = (cone & 1) ? -1 : 1;
-    const int base = alongx ? x : y;
-    const int nline = alongx ? d.nx : d.ny;
-    const int center = alongx ? y : x;
-    const int lim = alongx ? d.ny : d.nx;
-    for (int k = 1; k <= lp.neg_cells; ++k) {
-      const int line = base + sgn * k;
-      if ((unsigned)line >= (unsigned)nline) break;  // further rings are outside too
-      const int lo = max(0, center - k), hi = min(lim - 1, center + k);
-      bool found;
-      if (alongx)
-        found = ring_line(out.colbits + (int64_t)line * WY, lo, hi, qs, line, d.nx, fmin, fmax,
-                          fcount);
+// a ring slot whose line lies outside the map completes its phase empty, so
+// every slot's phase parity stays (step / kNegRing) & 1
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kNegThreads) k_negative(const Dims d, const LayerParams lp,
+                                                          const LayerPtrs out, int T) {
+  extern __shared__ __align__(16) int32_t sm[];
+  __shared__ __align__(8) uint64_t bars[kNegRing];
+  const int cone = blockIdx.y;               // 0:+x 1:-x 2:+y 3:-y
+  const bool alongx = cone < 2;              // sweep over x (lines = columns)
+  const int dir = (cone & 1) ? -1 : 1;       // ring lines lie at p + dir*k
+  const int A = alongx ? d.nx : d.ny;        // lines
+  const int B = alongx ? d.ny : d.nx;        // cross positions per line
+  const int K = lp.neg_cells;
+  const int NB = B + 2 * K + 2;              // apex cross positions -K-1 .. B+K
+  const int BP = (B + 3) & ~3;               // ring line stride (16-byte rows)
+  int32_t* ring = sm;                        // [kNegRing][BP]
+  int32_t* Dp = ring + kNegRing * BP;        // state of the previous line
+  int32_t* Dn = Dp + NB;
+  int32_t* Mnp = Dn + NB;
+  int32_t* Mnn = Mnp + NB;
+  int32_t* Mxp = Mnn + NB;
+  int32_t* Mxn = Mxp + NB;
+  const int32_t* __restrict__ src = alongx ? out.qsT : out.qs;  // line-contiguous
+  const int INF = K + 1;
+  const int p0 = blockIdx.x * T;             // tile lines [p0, p0+T)
+  if (p0 >= A) return;                       // grid sized for max(nx, ny)
+  const int p1 = min(A, p0 + T);
+  int pstart, nsteps;                        // apex lines, in sweep order
+  if (dir > 0) {
+    pstart = min(A - 1, p1 - 1 + K);
+    nsteps = pstart - p0 + 1;
+  } else {
+    pstart = max(0, p0 - K);
+    nsteps = p1 - pstart;
+  }
+  const bool tma = (B & 3) == 0;             // rows are whole 16-byte chunks
+  const uint32_t line_bytes = (uint32_t)B * 4u;
+  // step s reads ring-1 line pl(s) = pstart - dir*s + dir
+  auto line_of = [&](int st) { return pstart - dir * st + dir; };
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) {
+    Dp[i] = Dn[i] = INF;  // both buffers: guard cells are never rewritten
+    Mnp[i] = Mnn[i] = INT32_MAX;
+    Mxp[i] = Mxn[i] = INT32_MIN;
+  }
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kNegRing; ++j) mbar_init(&bars[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tma && threadIdx.x == 0) {
+    for (int j = 0; j < kNegRing && j < nsteps; ++j) {
+      const int pl = line_of(j);
+      if (pl >= 0 && pl < A)
+        tma_line(ring + j * BP, src + (int64_t)pl * B, line_bytes, &bars[j]);
       else
-        found = ring_line(out.rowbits + (int64_t)line * WX, lo, hi, qs, (int64_t)d.nx * line, 1,
-                          fmin, fmax, fcount);
-      if (found) break;
+        mbar_arrive(&bars[j]);
     }
   }
-  smin[cone][tx] = fcount ? (int32_t)fmin : INT32_MAX;
-  smax[cone][tx] = fcount ? (int32_t)fmax : INT32_MIN;
-  scnt[cone][tx] = (int32_t)fcount;
-  __syncthreads();
-  if (cone == 0 && c < cells) {
-    int32_t mn = smin[0][tx], mx = smax[0][tx], n = scnt[0][tx];
-#pragma unroll
-    for (int j = 1; j < 4; ++j) {
-      mn = min(mn, smin[j][tx]);
-      mx = max(mx, smax[j][tx]);
-      n += scnt[j][tx];
+  for (int st = 0; st < nsteps; ++st) {
+    const int p = pstart - dir * st;
+    const int pl = p + dir;
+    const bool inmap = pl >= 0 && pl < A;
+    const int j = st % kNegRing;
+    int32_t* lq = ring + j * BP;
+    if (inmap) {
+      if (tma) {
+        mbar_wait(&bars[j], (uint32_t)((st / kNegRing) & 1));
+      } else {
+        for (int b = threadIdx.x; b < B; b += blockDim.x) lq[b] = __ldg(src + (int64_t)pl * B + b);
+        __syncthreads();
+      }
     }
-    out.neg[c] = (undef && n >= 2 && (int64_t)mx - (int64_t)mn > lp.T_neg) ? 1 : 0;
+    for (int i = threadIdx.x + 1; i < NB - 1; i += blockDim.x) {
+      const int b = i - K - 1;  // apex cross position
+      int Dv = INF, mn = INT32_MAX, mx = INT32_MIN;
+      if (inmap) {  // ring 1: cross b-1..b+1 of line pl (in-map only)
+#pragma unroll
+        for (int t = -1; t <= 1; ++t) {
+          const int bb = b + t;
+          if (bb >= 0 && bb < B) {
+            const int32_t q = lq[bb];
+            if (q != kQsUndef) {
+              Dv = 1;
+              mn = min(mn, q);
+              mx = max(mx, q);
+            }
+          }
+        }
+      }
+      if (Dv != 1) {
+        const int d0 = Dp[i - 1], d1 = Dp[i], d2 = Dp[i + 1];
+        const int dm = min(d0, min(d1, d2));
+        if (dm < K) {
+          Dv = dm + 1;
+          if (d0 == dm) { mn = min(mn, Mnp[i - 1]); mx = max(mx, Mxp[i - 1]); }
+          if (d1 == dm) { mn = min(mn, Mnp[i]); mx = max(mx, Mxp[i]); }
+          if (d2 == dm) { mn = min(mn, Mnp[i + 1]); mx = max(mx, Mxp[i + 1]); }
+        }
+      }
+      Dn[i] = Dv;
+      Mnn[i] = mn;
+      Mxn[i] = mx;
+      if (Dv <= K && b >= 0 && b < B && p >= p0 && p < p1) {
+        const int64_t cell = alongx ? (int64_t)b * d.nx + p : (int64_t)p * d.nx + b;
+        atomicMin(out.nmin + cell, mn);
+        atomicMax(out.nmax + cell, mx);
+      }
+    }
+    __syncthreads();  // state + ring slot j fully consumed
+    if (tma && threadIdx.x == 0 && st + kNegRing < nsteps) {
+      const int pn = line_of(st + kNegRing);
+      if (pn >= 0 && pn < A)
+        tma_line(lq, src + (int64_t)pn * B, line_bytes, &bars[j]);
+      else
+        mbar_arrive(&bars[j]);
+    }
+    int32_t* t0 = Dp; Dp = Dn; Dn = t0;
+    t0 = Mnp; Mnp = Mnn; Mnn = t0;
+    t0 = Mxp; Mxp = Mxn; Mxn = t0;
   }
 }
 
@@ -463,20 +570,34 @@ inline unsigned cells_blocks(const Dims& d, int tpb) {
 
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
                            const LayerPtrs& out, cudaStream_t st) {
-  const int64_t warps = (int64_t)d.nx * d.ny;
-  k_columns<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(ss, d, lp, out);
+  const int64_t lanes = ((int64_t)d.nx * d.ny) << ss.kp_log2;
+  k_columns<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st) {
-  k_slope<<<cells_blocks(d, 128), 128, 0, st>>>(d, lp, out);
+  const dim3 grid((d.nx + kSlopeTX - 1) / kSlopeTX, (d.ny + kSlopeTY - 1) / kSlopeTY);
+  k_slope<<<grid, dim3(kSlopeTX, kSlopeTY), 0, st>>>(d, lp, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                             cudaStream_t st) {
-  k_negative<<<cells_blocks(d, 32), dim3(32, 4), 0, st>>>(d, lp, out);
+  const int A = d.nx > d.ny ? d.nx : d.ny, B = A;
+  // tiles: about one block per SM over the 4 cones, at least 8 lines each
+  int T = (4 * A + 147) / 148;
+  T = T < 8 ? 8 : ((T + 7) / 8) * 8;
+  const size_t NB = (size_t)B + 2 * (size_t)lp.neg_cells + 2;
+  const size_t BP = ((size_t)B + 3) & ~(size_t)3;
+  const size_t smem = sizeof(int32_t) * (6 * NB + kNegRing * BP);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        k_negative, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid((unsigned)((A + T - 1) / T), 4);
+  k_negative<<<grid, kNegThreads, smem, st>>>(d, lp, out, T);
   return cudaGetLastError();
 }
 
