@@ -11,6 +11,7 @@
 // the voxel walk is bit-identical to the oracle's.  Integer accumulation only
 // (u32/u64 atomics): results are independent of thread schedule.
 #include <cuda/atomic>
+#include <stdlib.h>
 
 #include "gvom_internal.cuh"
 
@@ -86,36 +87,42 @@ __device__ void walk_exact(const int S[3], const int E[3], const float g[3], con
   }
 }
 
-// Per-axis DDA setup (O5).  The stateless key of the oracle,
-//   key_a(V) = f32( f32( f32(V_a + [step_a>0]) - s_a ) * inv_a ),
-// is evaluated from a float edge e_a = f32(V_a + [step_a>0]) that moves by
-// exactly +-1 (integers < 2^24), so it is bit-identical.  Gating: an axis
-// with no steps left carries key +inf; with every live key finite this picks
-// exactly the oracle's argmin (strict <, ties to the lowest axis).
-//   exit axis (the walk leaves the grid through it): c = in-grid steps left;
-//   selecting it with c == 0 ends the walk.
-//   other axes: c = rem; the key becomes +inf when c reaches 0.
-__device__ __forceinline__ void axis_setup(int S, int E, float g, float s, int n, int stride,
-                                           float& e, float& f, float& inv, float& key, int& c,
-                                           int& dL, bool& x, int& rem, bool& finite) {
-  const int st = (E > S) - (E < S);
-  rem = abs(E - S);
-  const int room = st > 0 ? (n - 1 - S) : S;  // in-grid steps available
-  f = (float)st;
-  // no steps on this axis: key (e - s) * inv = (S + 1 - s) * +inf = +inf
-  e = (float)(S + (st >= 0 ? 1 : 0));
-  inv = __int_as_float(0x7f800000);
-  key = __int_as_float(0x7f800000);
-  x = rem > room;
-  c = x ? room : rem;
-  if (rem > 0) {
-    inv = __frcp_rn(__fsub_rn(g, s));
-    key = __fmul_rn(__fsub_rn(e, s), inv);
-    finite = finite && isfinite(inv);
-  }
-  dL = st * stride;
+// key of the j-th crossing (j >= 1) of an axis: f32(f32(e_j - s) * inv) with
+// the exact float edge e_j = e1 + step*(j-1)  (O5's stateless key)
+__device__ __forceinline__ float axis_key(float e1, float f, float s, float inv, int j) {
+  return __fmul_rn(__fsub_rn(__fadd_rn(e1, f * (float)(j - 1)), s), inv);
 }
 
+// number of crossings j in [1, jmax] of an axis that precede (K, tie_ok):
+// key_j < K, or key_j == K with the axis ordered first.  Keys are monotone
+// non-decreasing in j, so this is a binary search.
+__device__ __forceinline__ int count_before(float e1, float f, float s, float inv, int jmax,
+                                            float K, bool tie_ok) {
+  int lo = 0, hi = jmax;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    const float k = axis_key(e1, f, s, inv, mid);
+    if (k < K || (k == K && tie_ok))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// (k, a) > (K, A) in the walk order (key, then axis index)
+__device__ __forceinline__ bool after(float k, int a, float K, int A) {
+  return k > K || (k == K && a > A);
+}
+
+// Ray cast (O5) for a frame's points.  The walk of a ray is the merge, in
+// (key, axis) order, of its three monotone per-axis crossing sequences.  At
+// setup each lane computes its exact walk length T (the emits: sum rem_a, or
+// 1 + the crossings before the first grid-exit crossing, counted by binary
+// search) and checks that no exhausted axis's next key can precede the
+// walk's end; then it runs T ungated argmin steps.  Rays failing the check or
+// with a non-finite 1/d take the exact slow path.  The rule is restated and
+// checked against the oracle in tests/test_dda_fastpath_rule.py.
 __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts, int64_t n,
                                                  int32_t rings, const SensorParams sp,
                                                  const Dims d, uint32_t* __restrict__ miss,
@@ -126,88 +133,144 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
   const float s0 = sp.b[0], s1 = sp.b[1], s2 = sp.b[2];
   const float kInf = __int_as_float(0x7f800000);
 
-  bool active = false;
   float e0 = 0.f, e1 = 0.f, e2 = 0.f, f0 = 0.f, f1 = 0.f, f2 = 0.f;
-  float i0 = 0.f, i1 = 0.f, i2 = 0.f, k0 = kInf, k1 = kInf, k2 = kInf;
-  int c0 = 0, c1 = 0, c2 = 0, dL0 = 0, dL1 = 0, dL2 = 0, left = 0;
-  bool x0 = false, x1 = false, x2 = false;
+  float i0 = kInf, i1 = kInf, i2 = kInf, k0 = kInf, k1 = kInf, k2 = kInf;
+  int dL0 = 0, dL1 = 0, dL2 = 0, left = 0;
   uint32_t L = 0;
 
   if (p < n) {
     const float4 q = __ldg(pts + p);
-    float g0, g1, g2;
-    if (transform_point(sp, q, g0, g1, g2)) {
-      const int E0 = (int)floorf(g0), E1 = (int)floorf(g1), E2 = (int)floorf(g2);
+    float g[3];
+    if (transform_point(sp, q, g[0], g[1], g[2])) {
+      const int n3[3] = {d.nx, d.ny, d.nz};
       const int strideY = d.nz * d.nx;
+      const int str[3] = {d.nz, strideY, 1};
+      const float s[3] = {s0, s1, s2};
+      int E[3], st[3], rem[3], room[3];
+      float eb[3], fb[3], inv[3];
+      bool fin = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        E[a] = (int)floorf(g[a]);
+        st[a] = (E[a] > sp.S[a]) - (E[a] < sp.S[a]);
+        rem[a] = abs(E[a] - sp.S[a]);
+        room[a] = st[a] > 0 ? (n3[a] - 1 - sp.S[a]) : sp.S[a];
+        fb[a] = (float)st[a];
+        eb[a] = (float)(sp.S[a] + (st[a] >= 0 ? 1 : 0));
+        inv[a] = kInf;
+        if (rem[a] > 0) {
+          inv[a] = __frcp_rn(__fsub_rn(g[a], s[a]));
+          fin = fin && isfinite(inv[a]);
+        }
+      }
       // endpoint occupancy (O4/O6: occupied iff hits >= 1)
-      if ((unsigned)E0 < (unsigned)d.nx && (unsigned)E1 < (unsigned)d.ny &&
-          (unsigned)E2 < (unsigned)d.nz) {
-        const uint32_t LE = (uint32_t)(E2 + d.nz * E0 + strideY * E1);
+      if ((unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
+          (unsigned)E[2] < (unsigned)d.nz) {
+        const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
         atomicOr(bits + (LE >> 5), 1u << (LE & 31));
       }
-      int r0, r1, r2;
-      bool fin = true;
-      axis_setup(sp.S[0], E0, g0, s0, d.nx, d.nz, e0, f0, i0, k0, c0, dL0, x0, r0, fin);
-      axis_setup(sp.S[1], E1, g1, s1, d.ny, strideY, e1, f1, i1, k1, c1, dL1, x1, r1, fin);
-      axis_setup(sp.S[2], E2, g2, s2, d.nz, 1, e2, f2, i2, k2, c2, dL2, x2, r2, fin);
-      L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]);
-      // steps until E when no axis exits the grid; otherwise the exit ends it
-      // (a walk never takes more than nx+ny+nz in-grid steps: hard cap)
-      left = (x0 || x1 || x2) ? d.nx + d.ny + d.nz : r0 + r1 + r2;
-      active = (r0 | r1 | r2) != 0;  // the sensor voxel is in the grid (host check)
-      if (active && !fin) {
-        const int S[3] = {sp.S[0], sp.S[1], sp.S[2]}, E[3] = {E0, E1, E2};
-        const float g[3] = {g0, g1, g2}, s[3] = {s0, s1, s2};
-        walk_exact(S, E, g, s, d, miss);
-        active = false;
+      const int R = rem[0] + rem[1] + rem[2];
+      if (R > 0) {
+        bool ok = fin;
+        float Kend = 0.f;
+        int Aend = -1;
+        bool anyexit = false;
+        if (ok) {
+          // first exit crossing (key, axis)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (rem[a] > room[a]) {
+              const float kx = axis_key(eb[a], fb[a], s[a], inv[a], room[a] + 1);
+              if (!anyexit || kx < Kend) {
+                Kend = kx;
+                Aend = a;
+              }
+              anyexit = true;
+            }
+          }
+          if (anyexit) {
+            int T = 1;
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              if (b == Aend)
+                T += room[b];
+              else if (rem[b] > 0)
+                T += count_before(eb[b], fb[b], s[b], inv[b], min(rem[b], room[b] + 1), Kend,
+                                  b < Aend);
+            }
+            left = T;
+          } else {
+            left = R;
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              if (rem[b] > 0) {
+                const float kl = axis_key(eb[b], fb[b], s[b], inv[b], rem[b]);
+                if (Aend < 0 || after(kl, b, Kend, Aend)) {
+                  Kend = kl;
+                  Aend = b;
+                }
+              }
+            }
+          }
+          // no exhausted axis may become the argmin before the walk ends
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (rem[a] > 0 && rem[a] <= room[a]) {
+              const float ov = axis_key(eb[a], fb[a], s[a], inv[a], rem[a] + 1);
+              ok = ok && after(ov, a, Kend, Aend);
+            }
+          }
+        }
+        if (!ok) {
+          const int S[3] = {sp.S[0], sp.S[1], sp.S[2]};
+          walk_exact(S, E, g, s, d, miss);
+          left = 0;
+        } else {
+          e0 = eb[0]; e1 = eb[1]; e2 = eb[2];
+          f0 = fb[0]; f1 = fb[1]; f2 = fb[2];
+          i0 = inv[0]; i1 = inv[1]; i2 = inv[2];
+          k0 = rem[0] > 0 ? axis_key(eb[0], fb[0], s0, i0, 1) : kInf;
+          k1 = rem[1] > 0 ? axis_key(eb[1], fb[1], s1, i1, 1) : kInf;
+          k2 = rem[2] > 0 ? axis_key(eb[2], fb[2], s2, i2, 1) : kInf;
+          dL0 = st[0] * str[0];
+          dL1 = st[1] * str[1];
+          dL2 = st[2] * str[2];
+          L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]);
+        }
       }
     }
   }
 
-  const unsigned after = 0xfffffffeu << lane;  // lanes above this one
-  unsigned act = __ballot_sync(0xffffffffu, active);
+  const unsigned after_lanes = 0xfffffffeu << lane;  // lanes above this one
+  unsigned act = __ballot_sync(0xffffffffu, left > 0);
   while (act) {
+    const bool active = left > 0;
     // Merge equal voxels of adjacent lanes: one atomic per run of lanes.
     const uint32_t key = active ? L : 0xffffffffu;
     const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
     const bool head = active && (lane == 0 || prev != key);
     const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after)) - lane);
+    const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
     asm volatile(
         "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
         "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
         "r"(cnt), "r"((uint32_t)head)
         : "memory");
-    // One DDA step for every lane; inactive lanes compute values that are
-    // never emitted (`active` only goes from true to false).
+    // argmin, strict <, ties to the lowest axis (O5); no gating needed
     const bool l10 = k1 < k0;
     const float b01 = l10 ? k1 : k0;
     const bool u2 = k2 < b01;
     const bool u1 = l10 && !u2;
     const bool u0 = !l10 && !u2;
-    const int cs = u2 ? c2 : (u1 ? c1 : c0);
-    const bool xs = u2 ? x2 : (u1 ? x1 : x0);
-    const bool out = xs && cs == 0;  // this step would leave the grid
     e0 = u0 ? __fadd_rn(e0, f0) : e0;
     e1 = u1 ? __fadd_rn(e1, f1) : e1;
     e2 = u2 ? __fadd_rn(e2, f2) : e2;
-    c0 -= u0;
-    c1 -= u1;
-    c2 -= u2;
     L += (uint32_t)(u2 ? dL2 : (u1 ? dL1 : dL0));
-    // A non-exit axis that used its last step gets 1/d = +-inf: its key
-    // (e - s) * inv is then +inf for good (e - s is nonzero with the sign of
-    // the step once the axis has moved).
-    const bool exh = !xs && cs == 1;
-    i0 = (u0 && exh) ? f0 * kInf : i0;
-    i1 = (u1 && exh) ? f1 * kInf : i1;
-    i2 = (u2 && exh) ? f2 * kInf : i2;
     k0 = __fmul_rn(__fsub_rn(e0, s0), i0);
     k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
     k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
     --left;
-    active = active && !out && left != 0;
-    act = __ballot_sync(0xffffffffu, active);
+    act = __ballot_sync(0xffffffffu, left > 0);
   }
 }
 
@@ -532,8 +595,15 @@ cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const Se
                            const Dims& d, uint32_t* miss_grid, uint32_t* bits, cudaStream_t st) {
   const int64_t threads = point_threads(n, rings);
   if (threads == 0) return cudaSuccess;
-  const int64_t blocks = (threads + 255) / 256;
-  k_raycast<<<(unsigned)blocks, 256, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits);
+  // small blocks: a frame is one wave of warps; many small blocks spread the
+  // long (upward / horizontal) and short (ground) rings evenly over the SMs
+  static const int bs = [] {
+    const char* e = getenv("GVOM_RAY_BLOCK");
+    const int v = e ? atoi(e) : 64;
+    return (v >= 32 && v <= 256 && v % 32 == 0) ? v : 64;
+  }();
+  const int64_t blocks = (threads + bs - 1) / bs;
+  k_raycast<<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits);
   return cudaGetLastError();
 }
 
