@@ -180,8 +180,9 @@ GVOM_API gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_vox
 GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_voxel* d_data,
                               int64_t cap, int64_t* out_k, int64_t out_origin[3]);
 
-/* Instrumentation.  With timing enabled every kernel launch is bracketed by
- * CUDA events on the handle's stream; gvom_stage_times synchronises and
+/* Instrumentation.  gvom_set_timing(h, mask): every launch of a stage whose
+ * bit (1 << GVOM_STAGE_*) is set in mask is bracketed by CUDA events on the
+ * handle's stream (mask -1 = all stages, 0 = off); gvom_stage_times synchronises and
  * returns, per stage, [total ms, launches] pairs (2*GVOM_STAGE_COUNT
  * doubles), then clears the record.  gvom_launch_count returns the number of
  * kernels this handle has launched so far.                                  */

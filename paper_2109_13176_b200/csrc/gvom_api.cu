@@ -31,7 +31,7 @@ struct Slot {
 
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
-  size_t staging, rank_tmp, rank_status, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
+  size_t staging, rank_tmp, rank_status, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
       total;
   int64_t cap, nblk, cells;
 };
@@ -83,6 +83,9 @@ Layout make_layout(const gvom_config* c) {
   off += align_up(4 * (size_t)(l.nblk + 2));
   l.rank_status = off;  // [0] ticket counter, [1 + b] tile status (decoupled look-back)
   off += align_up(8 * (size_t)(l.nblk + 1));
+  l.tilecnt = off;  // occupancy counts per finalize tile, then per super-tile
+  l.tilecnt_bytes = align_up(4 * (size_t)(n_tiles(d) + n_supers(d)));
+  off += l.tilecnt_bytes;
   l.layers_f32 = off;  // height, density, slope, rough
   off += 4 * align_up(4 * (size_t)l.cells);
   l.layers_u8 = off;  // hard, soft, neg
@@ -130,6 +133,8 @@ struct gvom_handle {
   std::vector<cudaEvent_t> pool;
   int64_t launches = 0;
   uint64_t rank_calls = 0;  // decoupled look-back epochs / ticket base
+  uint32_t timing_mask = 0;  // stages bracketed by CUDA events
+  TileCounts tc{};
 };
 
 namespace {
@@ -149,13 +154,14 @@ cudaEvent_t take_event(gvom_handle* h) {
 template <class F>
 cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f) {
   cudaEvent_t a = nullptr, b = nullptr;
-  if (h->timing) {
+  const bool timed = h->timing && ((h->timing_mask >> id) & 1u);
+  if (timed) {
     a = take_event(h);
     b = take_event(h);
     if (a) cudaEventRecord(a, h->st);
   }
   const cudaError_t e = f();
-  if (h->timing && a && b) {
+  if (timed && a && b) {
     cudaEventRecord(b, h->st);
     h->recs.push_back({id, a, b});
   }
@@ -314,6 +320,8 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.nmin = (int32_t*)(h->ws + lay.defbits + align_up(4 * (size_t)lay.cells));
   h->layers.nmax = (int32_t*)(h->ws + lay.defbits + 2 * align_up(4 * (size_t)lay.cells));
   h->mbits = (uint32_t*)(h->ws + lay.mbits);
+  h->tc.tile = (uint32_t*)(h->ws + lay.tilecnt);
+  h->tc.super = h->tc.tile + n_tiles(h->d);
   h->mprefix = (uint32_t*)(h->ws + lay.mprefix);
   // integer thresholds
   h->lp.T_lo = llround(cfg->min_obstacle_height / cfg->res * 65536.0);
@@ -393,8 +401,9 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
-    return launch_zero2(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
-                        (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->st);
+    return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
+                        (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
+                        h->lay.tilecnt_bytes, h->st);
   }));
   // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
   std::vector<const float4*> dptr(n_scans);
@@ -417,14 +426,13 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     }
     GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
       return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits,
-                            h->st);
+                            h->tc, h->st);
     }));
   }
   // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
-  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true,
-                [&] { return run_rank(h, slot.bits, slot.wprefix, slot.meta); }));
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
-    return launch_finalize(slot.lut, slot.bits, slot.wprefix, slot.data, d, h->st);
+    return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, h->tc, slot.meta,
+                                 d, h->st);
   }));
   // pass 2b: per-return metrics into the data rows
   for (int i = 0; i < n_scans; ++i) {
@@ -570,6 +578,7 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
 gvom_status gvom_set_timing(gvom_handle* h, int32_t enable) {
   if (!h) return GVOM_E_INVALID;
   h->timing = enable != 0;
+  h->timing_mask = enable == -1 ? 0xffffffffu : (uint32_t)enable;
   return GVOM_OK;
 }
 

@@ -9,6 +9,9 @@
 
 namespace gvom {
 
+constexpr int kTileWords = 256;           // finalize tile: 256 words = 8192 voxels
+constexpr int kTileShift = 13;            // voxel L -> tile
+constexpr int kSuperShift = 19;           // voxel L -> super-tile (64 tiles)
 constexpr int kRankWordsPerBlock = 1024;  // bitmask words per rank tile (32768 voxels)
 constexpr int kRankThreads = 256;         // 4 words per thread
 constexpr uint32_t kMissSat = 1u << 30;   // A11
@@ -65,8 +68,21 @@ struct LayerParams {
 };
 
 // ---- launchers (each launches exactly one kernel; returns cudaError_t) ----
+// occupancy counters per tile / super-tile, kept by the ray cast as bits are set
+struct TileCounts {
+  uint32_t* tile;
+  uint32_t* super;
+};
+__host__ __device__ inline int64_t n_tiles(const Dims& d) { return (d.V + (1 << kTileShift) - 1) >> kTileShift; }
+__host__ __device__ inline int64_t n_supers(const Dims& d) { return (d.V + (1 << kSuperShift) - 1) >> kSuperShift; }
+
 cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                           const Dims& d, uint32_t* miss_grid, uint32_t* bits, cudaStream_t st);
+                           const Dims& d, uint32_t* miss_grid, uint32_t* bits,
+                           const TileCounts& tc, cudaStream_t st);
+// rank (from the tile counts) + in-place LUT encode + data-row init, one launch
+cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
+                                  gvom_voxel* data, const TileCounts& tc, uint32_t* total,
+                                  const Dims& d, cudaStream_t st);
 cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
                               cudaStream_t st);
 cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
@@ -76,8 +92,9 @@ cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const ui
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st);
-// zeroes a[0:abytes) and b[0:bbytes) (sizes multiples of 16, 16-byte aligned)
-cudaError_t launch_zero2(void* a, size_t abytes, void* b, size_t bbytes, cudaStream_t st);
+// zeroes a[0:abytes), b[0:bbytes), c[0:cbytes) (multiples of 16, 16-byte aligned)
+cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
+                         cudaStream_t st);
 cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
                                const Dims& d, cudaStream_t st);
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,

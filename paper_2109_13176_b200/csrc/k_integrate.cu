@@ -126,7 +126,8 @@ __device__ __forceinline__ bool after(float k, int a, float K, int A) {
 __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts, int64_t n,
                                                  int32_t rings, const SensorParams sp,
                                                  const Dims d, uint32_t* __restrict__ miss,
-                                                 uint32_t* __restrict__ bits) {
+                                                 uint32_t* __restrict__ bits,
+                                                 const TileCounts tc) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t p = point_index(tid, rings);
   const int lane = threadIdx.x & 31;
@@ -167,7 +168,11 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
       if ((unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
           (unsigned)E[2] < (unsigned)d.nz) {
         const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
-        atomicOr(bits + (LE >> 5), 1u << (LE & 31));
+        const uint32_t bit = 1u << (LE & 31);
+        if (!(atomicOr(bits + (LE >> 5), bit) & bit)) {  // newly occupied voxel
+          atomicAdd(tc.tile + (LE >> kTileShift), 1u);
+          atomicAdd(tc.super + (LE >> kSuperShift), 1u);
+        }
       }
       const int R = rem[0] + rem[1] + rem[2];
       if (R > 0) {
@@ -529,16 +534,110 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(const uint32_t* __restric
   }
 }
 
-// Zero two regions in one launch (the slot's LUT-as-miss-grid and bitmask).
-__global__ void __launch_bounds__(256) k_zero2(uint4* __restrict__ a, int64_t na16,
-                                               uint4* __restrict__ b, int64_t nb16) {
+// Zero three regions in one launch (the slot's LUT-as-miss-grid, its
+// occupancy bitmask, and the tile counters).
+__global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na,
+                                               uint4* __restrict__ b, int64_t nb,
+                                               uint4* __restrict__ c, int64_t nc) {
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na16 + nb16; i += stride) {
-    if (i < na16)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb + nc; i += stride) {
+    if (i < na)
       __stcs(a + i, z);
+    else if (i < na + nb)
+      __stcs(b + (i - na), z);
     else
-      __stcs(b + (i - na16), z);
+      __stcs(c + (i - na - nb), z);
+  }
+}
+
+// Rank + O6 encode in one launch.  Block b owns tile b (256 bitmask words =
+// 8192 voxels): its rank offset is the sum of the super-tile counts before
+// its super-tile plus the tile counts before it inside it (both kept by the
+// ray cast), so no block waits on another.  Then: per-word prefix (block
+// scan), wprefix store, and the in-place LUT encode / data-row init of its
+// 8192 voxels with 16-byte accesses.
+__global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
+    int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
+    gvom_voxel* __restrict__ data, const TileCounts tc, uint32_t* __restrict__ total,
+    const Dims d) {
+  __shared__ uint32_t sbits[kTileWords], spre[kTileWords], wsum[kTileWords / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t b = blockIdx.x;
+  const int64_t sb = b >> (kSuperShift - kTileShift);
+  // rank offset of this tile
+  uint32_t part = 0;
+  for (int64_t i = t; i < sb; i += kTileWords) part += __ldg(tc.super + i);
+  for (int64_t i = (sb << (kSuperShift - kTileShift)) + t; i < b; i += kTileWords)
+    part += __ldg(tc.tile + i);
+  part = __reduce_add_sync(0xffffffffu, part);
+  if (lane == 0) wsum[wid] = part;
+  __syncthreads();
+  uint32_t off = 0;
+#pragma unroll
+  for (int i = 0; i < kTileWords / 32; ++i) off += wsum[i];
+  __syncthreads();
+  if (b == 0 && t == 0) {  // k = all occupied voxels
+    uint32_t k = 0;
+    for (int64_t i = 0; i < n_supers(d); ++i) k += __ldg(tc.super + i);
+    *total = k;
+  }
+  // per-word exclusive prefix within the tile
+  const int64_t w = b * kTileWords + t;
+  const uint32_t bw = w < d.W ? __ldg(bits + w) : 0u;
+  const uint32_t c = __popc(bw);
+  const uint32_t inc = warp_incl_scan(c, lane);
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = lane < kTileWords / 32 ? wsum[lane] : 0u;
+    const uint32_t e = warp_incl_scan(v, lane) - v;
+    if (lane < kTileWords / 32) wsum[lane] = e;
+  }
+  __syncthreads();
+  const uint32_t pre = off + wsum[wid] + inc - c;
+  sbits[t] = bw;
+  spre[t] = pre;
+  if (w < d.W) wprefix[w] = pre;
+  __syncthreads();
+  // voxels of the tile, 4 per thread per iteration
+  const int64_t vbase = b << kTileShift;
+  for (int i = t * 4; i < (1 << kTileShift); i += kTileWords * 4) {
+    const int64_t L = vbase + i;
+    if (L >= d.V) break;
+    const uint32_t ww = sbits[i >> 5], pp = spre[i >> 5];
+    const bool vec = (L + 3 < d.V);
+    uint32_t m[4];
+    if (vec) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(buf + L));
+      m[0] = v.x;
+      m[1] = v.y;
+      m[2] = v.z;
+      m[3] = v.w;
+    } else {
+      for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
+    }
+    int32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int bit = (i + j) & 31;
+      if ((ww >> bit) & 1u) {
+        const uint32_t rank = pp + __popc(ww & ((1u << bit) - 1u));
+        o[j] = (int32_t)rank;
+        uint4* row = reinterpret_cast<uint4*>(data + rank);
+        row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
+        row[1] = make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        const uint32_t nm = m[j] < kMissSat ? m[j] : kMissSat;
+        o[j] = -1 - (int32_t)nm;
+      }
+    }
+    if (vec) {
+      *reinterpret_cast<int4*>(buf + L) = make_int4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int j = 0; j < 4; ++j)
+        if (L + j < d.V) buf[L + j] = o[j];
+    }
   }
 }
 
@@ -555,31 +654,61 @@ __global__ void __launch_bounds__(kRankThreads) k_prefix_only(const uint32_t* __
 }
 
 // O4 per return: hits, min_dz, m1 = sum dz, m2 = sum dz^2 into the data row.
+// Returns of azimuth-adjacent lanes often share a voxel (ground near the
+// sensor): runs of equal voxels are reduced with a segmented shuffle
+// reduction and the run head issues the four atomics.
 __global__ void __launch_bounds__(256) k_endpoint(const float4* __restrict__ pts, int64_t n,
                                                   int32_t rings, const SensorParams sp,
                                                   const Dims d, const int32_t* __restrict__ lut,
                                                   gvom_voxel* __restrict__ data) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t p = point_index(tid, rings);
-  if (p >= n) return;
-  const float4 q = __ldg(pts + p);
-  float g0, g1, g2;
-  if (!transform_point(sp, q, g0, g1, g2)) return;
-  const int e0 = (int)floorf(g0), e1 = (int)floorf(g1), e2 = (int)floorf(g2);
-  if ((unsigned)e0 >= (unsigned)d.nx || (unsigned)e1 >= (unsigned)d.ny ||
-      (unsigned)e2 >= (unsigned)d.nz)
-    return;
-  const int64_t LE = (int64_t)e2 + (int64_t)d.nz * e0 + (int64_t)d.nz * d.nx * e1;
-  const int32_t rank = __ldg(lut + LE);
-  // qz = floor(f32(g_z * 65536)) is exact (power-of-two scale)
-  const int64_t qz = (int64_t)floorf(__fmul_rn(g2, 65536.0f));
-  const uint32_t dz = (uint32_t)(qz - 65536ll * e2);
-  gvom_voxel* row = data + rank;
-  atomicAdd(&row->hits, 1u);
-  atomicMin(&row->min_dz, dz);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&row->m1), (unsigned long long)dz);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&row->m2),
-            (unsigned long long)dz * (unsigned long long)dz);
+  const int lane = threadIdx.x & 31;
+  bool valid = false;
+  uint32_t LE = 0xffffffffu, dz = 0u;
+  if (p < n) {
+    const float4 q = __ldg(pts + p);
+    float g0, g1, g2;
+    if (transform_point(sp, q, g0, g1, g2)) {
+      const int e0 = (int)floorf(g0), e1 = (int)floorf(g1), e2 = (int)floorf(g2);
+      if ((unsigned)e0 < (unsigned)d.nx && (unsigned)e1 < (unsigned)d.ny &&
+          (unsigned)e2 < (unsigned)d.nz) {
+        valid = true;
+        LE = (uint32_t)(e2 + d.nz * e0 + d.nz * d.nx * e1);
+        // qz = floor(f32(g_z * 65536)) is exact (power-of-two scale)
+        const int64_t qz = (int64_t)floorf(__fmul_rn(g2, 65536.0f));
+        dz = (uint32_t)(qz - 65536ll * e2);
+      }
+    }
+  }
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (act == 0u) return;  // warp-uniform
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, LE, 1);
+  const bool head = valid && (lane == 0 || prev != LE);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const int end = __clz(__brev((heads | ~act) & (0xfffffffeu << lane))) - 1;  // run's last lane
+  uint32_t cnt = valid ? 1u : 0u, s1 = dz, mn = valid ? dz : 0xffffffffu;
+  uint64_t s2 = (uint64_t)dz * dz;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t c_o = __shfl_down_sync(0xffffffffu, cnt, o);
+    const uint32_t s1_o = __shfl_down_sync(0xffffffffu, s1, o);
+    const uint64_t s2_o = __shfl_down_sync(0xffffffffu, s2, o);
+    const uint32_t mn_o = __shfl_down_sync(0xffffffffu, mn, o);
+    if (lane + o <= end) {
+      cnt += c_o;
+      s1 += s1_o;
+      s2 += s2_o;
+      mn = min(mn, mn_o);
+    }
+  }
+  if (head) {
+    gvom_voxel* row = data + __ldg(lut + LE);
+    atomicAdd(&row->hits, cnt);
+    atomicMin(&row->min_dz, mn);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&row->m1), (unsigned long long)s1);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&row->m2), (unsigned long long)s2);
+  }
 }
 
 inline int64_t point_threads(int64_t n, int32_t rings) {
@@ -592,7 +721,8 @@ inline int64_t point_threads(int64_t n, int32_t rings) {
 }  // namespace
 
 cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                           const Dims& d, uint32_t* miss_grid, uint32_t* bits, cudaStream_t st) {
+                           const Dims& d, uint32_t* miss_grid, uint32_t* bits,
+                           const TileCounts& tc, cudaStream_t st) {
   const int64_t threads = point_threads(n, rings);
   if (threads == 0) return cudaSuccess;
   // small blocks: a frame is one wave of warps; many small blocks spread the
@@ -603,7 +733,7 @@ cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const Se
     return (v >= 32 && v <= 256 && v % 32 == 0) ? v : 64;
   }();
   const int64_t blocks = (threads + bs - 1) / bs;
-  k_raycast<<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits);
+  k_raycast<<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits, tc);
   return cudaGetLastError();
 }
 
@@ -636,13 +766,23 @@ cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_zero2(void* a, size_t abytes, void* b, size_t bbytes, cudaStream_t st) {
-  const int64_t n = (int64_t)(abytes / 16 + bbytes / 16);
+cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
+                         cudaStream_t st) {
+  const int64_t n = (int64_t)(abytes / 16 + bbytes / 16 + cbytes / 16);
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  k_zero2<<<(unsigned)blocks, 256, 0, st>>>((uint4*)a, (int64_t)(abytes / 16), (uint4*)b,
-                                            (int64_t)(bbytes / 16));
+  k_zero3<<<(unsigned)blocks, 256, 0, st>>>((uint4*)a, (int64_t)(abytes / 16), (uint4*)b,
+                                            (int64_t)(bbytes / 16), (uint4*)c,
+                                            (int64_t)(cbytes / 16));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
+                                  gvom_voxel* data, const TileCounts& tc, uint32_t* total,
+                                  const Dims& d, cudaStream_t st) {
+  k_finalize_tiles<<<(unsigned)n_tiles(d), kTileWords, 0, st>>>(lut_inplace, bits, wprefix, data,
+                                                                tc, total, d);
   return cudaGetLastError();
 }
 

@@ -294,8 +294,12 @@ class GvomMap:
         return lut.cpu().numpy(), self._split(data, k.value), np.array(o[:], dtype=np.int64)
 
     # -- instrumentation -----------------------------------------------------
-    def set_timing(self, enable: bool):
-        _check(self.lib.gvom_set_timing(self.h, 1 if enable else 0), "gvom_set_timing")
+    def set_timing(self, enable: bool = True, stages: Optional[Iterable[str]] = None):
+        """Bracket kernel launches with CUDA events: all stages, or only `stages`."""
+        mask = 0
+        if enable:
+            mask = -1 if stages is None else sum(1 << STAGES.index(s) for s in stages)
+        _check(self.lib.gvom_set_timing(self.h, mask), "gvom_set_timing")
 
     def stage_times(self) -> Dict[str, Tuple[float, int]]:
         buf = (C.c_double * (2 * len(STAGES)))()
