@@ -83,8 +83,8 @@ Layout make_layout(const gvom_config* c) {
   off += align_up(4 * (size_t)(l.nblk + 2));
   l.rank_status = off;  // [0] ticket counter, [1 + b] tile status (decoupled look-back)
   off += align_up(8 * (size_t)(l.nblk + 1));
-  l.tilecnt = off;  // occupancy counts per finalize tile, then per super-tile
-  l.tilecnt_bytes = align_up(4 * (size_t)(n_tiles(d) + n_supers(d)));
+  l.tilecnt = off;  // per finalize tile: occupancy counts, offsets; then the done counter
+  l.tilecnt_bytes = align_up(4 * (size_t)(2 * n_tiles(d) + 4));
   off += l.tilecnt_bytes;
   l.layers_f32 = off;  // height, density, slope, rough
   off += 4 * align_up(4 * (size_t)l.cells);
@@ -321,7 +321,8 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.nmax = (int32_t*)(h->ws + lay.defbits + 2 * align_up(4 * (size_t)lay.cells));
   h->mbits = (uint32_t*)(h->ws + lay.mbits);
   h->tc.tile = (uint32_t*)(h->ws + lay.tilecnt);
-  h->tc.super = h->tc.tile + n_tiles(h->d);
+  h->tc.offset = h->tc.tile + n_tiles(h->d);
+  h->tc.done = h->tc.offset + n_tiles(h->d);
   h->mprefix = (uint32_t*)(h->ws + lay.mprefix);
   // integer thresholds
   h->lp.T_lo = llround(cfg->min_obstacle_height / cfg->res * 65536.0);
@@ -406,6 +407,11 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
                         h->lay.tilecnt_bytes, h->st);
   }));
   // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
+  TileCounts tc = h->tc;
+  tc.total = slot.meta;
+  int last_scan = -1;
+  for (int i = 0; i < n_scans; ++i)
+    if (scans[i].n > 0) last_scan = i;
   std::vector<const float4*> dptr(n_scans);
   int64_t off = 0;
   for (int i = 0; i < n_scans; ++i) {
@@ -425,14 +431,13 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
       off += s.n;
     }
     GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
-      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits,
-                            h->tc, h->st);
+      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits, tc,
+                            i == last_scan, h->st);
     }));
   }
   // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
-    return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, h->tc, slot.meta,
-                                 d, h->st);
+    return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st);
   }));
   // pass 2b: per-return metrics into the data rows
   for (int i = 0; i < n_scans; ++i) {

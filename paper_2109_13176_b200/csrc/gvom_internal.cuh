@@ -11,7 +11,6 @@ namespace gvom {
 
 constexpr int kTileWords = 256;           // finalize tile: 256 words = 8192 voxels
 constexpr int kTileShift = 13;            // voxel L -> tile
-constexpr int kSuperShift = 19;           // voxel L -> super-tile (64 tiles)
 constexpr int kRankWordsPerBlock = 1024;  // bitmask words per rank tile (32768 voxels)
 constexpr int kRankThreads = 256;         // 4 words per thread
 constexpr uint32_t kMissSat = 1u << 30;   // A11
@@ -68,21 +67,25 @@ struct LayerParams {
 };
 
 // ---- launchers (each launches exactly one kernel; returns cudaError_t) ----
-// occupancy counters per tile / super-tile, kept by the ray cast as bits are set
+// Occupancy counts per finalize tile, kept by the ray cast as bits are set;
+// the frame's last ray-cast block turns them into exclusive offsets.
 struct TileCounts {
-  uint32_t* tile;
-  uint32_t* super;
+  uint32_t* tile;    // [n_tiles] newly occupied voxels per tile
+  uint32_t* offset;  // [n_tiles] exclusive prefix of tile
+  uint32_t* done;    // [1] finished ray-cast blocks (last-block scan)
+  uint32_t* total;   // k of the frame (slot meta), written by the scan
 };
-__host__ __device__ inline int64_t n_tiles(const Dims& d) { return (d.V + (1 << kTileShift) - 1) >> kTileShift; }
-__host__ __device__ inline int64_t n_supers(const Dims& d) { return (d.V + (1 << kSuperShift) - 1) >> kSuperShift; }
+__host__ __device__ inline int64_t n_tiles(const Dims& d) {
+  return (d.V + (1 << kTileShift) - 1) >> kTileShift;
+}
 
 cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
                            const Dims& d, uint32_t* miss_grid, uint32_t* bits,
-                           const TileCounts& tc, cudaStream_t st);
+                           const TileCounts& tc, bool last_sensor, cudaStream_t st);
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
-                                  gvom_voxel* data, const TileCounts& tc, uint32_t* total,
-                                  const Dims& d, cudaStream_t st);
+                                  gvom_voxel* data, const TileCounts& tc, const Dims& d,
+                                  cudaStream_t st);
 cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
                               cudaStream_t st);
 cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,

@@ -123,11 +123,75 @@ __device__ __forceinline__ bool after(float k, int a, float K, int A) {
 // walk's end; then it runs T ungated argmin steps.  Rays failing the check or
 // with a non-finite 1/d take the exact slow path.  The rule is restated and
 // checked against the oracle in tests/test_dda_fastpath_rule.py.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane);
+
+// The frame's last finishing ray-cast block (of the last sensor's launch)
+// turns the tile counts into exclusive offsets and the frame's k.
+__device__ void scan_tiles_if_last(const TileCounts& tc, const Dims& d) {
+  __shared__ bool last;
+  __shared__ uint32_t wsum[32], carry;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tc.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int64_t nt = n_tiles(d);
+  for (int64_t base = 0; base < nt; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < nt ? __ldcg(tc.tile + i) : 0u;
+    const uint32_t inc = warp_incl_scan(v, lane);
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t w = lane < nw ? wsum[lane] : 0u;
+      const uint32_t e = warp_incl_scan(w, lane) - w;
+      if (lane < nw) wsum[lane] = e;
+    }
+    __syncthreads();
+    const uint32_t ex = carry + wsum[wid] + inc - v;
+    if (i < nt) tc.offset[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+    __syncthreads();
+  }
+}
+
+// One miss increment per active lane at voxel L, merged across lanes that
+// hold the same voxel: one red.add per group (runs of adjacent lanes, or
+// arbitrary groups via match.any).
+template <bool kMatchAgg>
+__device__ __forceinline__ void aggregate_red(uint32_t* __restrict__ miss, uint32_t L, bool active,
+                                              unsigned act, unsigned after_lanes, int lane) {
+  const uint32_t key = active ? L : 0xffffffffu;
+  bool head;
+  uint32_t cnt;
+  if (kMatchAgg) {
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    head = active && lane == __ffs(peers) - 1;
+    cnt = (uint32_t)__popc(peers);
+  } else {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+    head = active && (lane == 0 || prev != key);
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
+  }
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
+      "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
+      "r"(cnt), "r"((uint32_t)head)
+      : "memory");
+}
+
+template <bool kMatchAgg, bool kAggFirst>
 __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts, int64_t n,
                                                  int32_t rings, const SensorParams sp,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
-                                                 const TileCounts tc) {
+                                                 const TileCounts tc, bool last_sensor) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t p = point_index(tid, rings);
   const int lane = threadIdx.x & 31;
@@ -138,6 +202,7 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
   float i0 = kInf, i1 = kInf, i2 = kInf, k0 = kInf, k1 = kInf, k2 = kInf;
   int dL0 = 0, dL1 = 0, dL2 = 0, left = 0;
   uint32_t L = 0;
+  uint32_t newtile = 0xffffffffu;  // tile of a voxel this lane newly occupied
 
   if (p < n) {
     const float4 q = __ldg(pts + p);
@@ -169,10 +234,7 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
           (unsigned)E[2] < (unsigned)d.nz) {
         const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
         const uint32_t bit = 1u << (LE & 31);
-        if (!(atomicOr(bits + (LE >> 5), bit) & bit)) {  // newly occupied voxel
-          atomicAdd(tc.tile + (LE >> kTileShift), 1u);
-          atomicAdd(tc.super + (LE >> kSuperShift), 1u);
-        }
+        newtile = (atomicOr(bits + (LE >> 5), bit) & bit) ? 0xffffffffu : (LE >> kTileShift);
       }
       const int R = rem[0] + rem[1] + rem[2];
       if (R > 0) {
@@ -246,22 +308,20 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
     }
   }
 
+  // tile occupancy counts, one atomic per group of lanes in the same tile
+  {
+    const unsigned peers = __match_any_sync(0xffffffffu, newtile);
+    if (newtile != 0xffffffffu && lane == __ffs(peers) - 1)
+      atomicAdd(tc.tile + newtile, (uint32_t)__popc(peers));
+  }
   const unsigned after_lanes = 0xfffffffeu << lane;  // lanes above this one
   unsigned act = __ballot_sync(0xffffffffu, left > 0);
   while (act) {
     const bool active = left > 0;
-    // Merge equal voxels of adjacent lanes: one atomic per run of lanes.
-    const uint32_t key = active ? L : 0xffffffffu;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = active && (lane == 0 || prev != key);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
-    asm volatile(
-        "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
-        "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
-        "r"(cnt), "r"((uint32_t)head)
-        : "memory");
-    // argmin, strict <, ties to the lowest axis (O5); no gating needed
+    const uint32_t Lc = L;  // this step's voxel
+    if (kAggFirst) aggregate_red<kMatchAgg>(miss, Lc, active, act, after_lanes, lane);
+    // DDA step: argmin, strict <, ties to the lowest axis (O5); no gating
+    // needed (see above)
     const bool l10 = k1 < k0;
     const float b01 = l10 ? k1 : k0;
     const bool u2 = k2 < b01;
@@ -275,8 +335,10 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
     k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
     k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
     --left;
+    if (!kAggFirst) aggregate_red<kMatchAgg>(miss, Lc, active, act, after_lanes, lane);
     act = __ballot_sync(0xffffffffu, left > 0);
   }
+  if (last_sensor) scan_tiles_if_last(tc, d);
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
@@ -559,29 +621,11 @@ __global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na
 // 8192 voxels with 16-byte accesses.
 __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
-    gvom_voxel* __restrict__ data, const TileCounts tc, uint32_t* __restrict__ total,
-    const Dims d) {
+    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d) {
   __shared__ uint32_t sbits[kTileWords], spre[kTileWords], wsum[kTileWords / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t b = blockIdx.x;
-  const int64_t sb = b >> (kSuperShift - kTileShift);
-  // rank offset of this tile
-  uint32_t part = 0;
-  for (int64_t i = t; i < sb; i += kTileWords) part += __ldg(tc.super + i);
-  for (int64_t i = (sb << (kSuperShift - kTileShift)) + t; i < b; i += kTileWords)
-    part += __ldg(tc.tile + i);
-  part = __reduce_add_sync(0xffffffffu, part);
-  if (lane == 0) wsum[wid] = part;
-  __syncthreads();
-  uint32_t off = 0;
-#pragma unroll
-  for (int i = 0; i < kTileWords / 32; ++i) off += wsum[i];
-  __syncthreads();
-  if (b == 0 && t == 0) {  // k = all occupied voxels
-    uint32_t k = 0;
-    for (int64_t i = 0; i < n_supers(d); ++i) k += __ldg(tc.super + i);
-    *total = k;
-  }
+  const uint32_t off = __ldg(tc.offset + b);  // rank offset of this tile
   // per-word exclusive prefix within the tile
   const int64_t w = b * kTileWords + t;
   const uint32_t bw = w < d.W ? __ldg(bits + w) : 0u;
@@ -599,6 +643,7 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
   sbits[t] = bw;
   spre[t] = pre;
   if (w < d.W) wprefix[w] = pre;
+  if (b == gridDim.x - 1 && t == kTileWords - 1) *tc.total = pre + c;  // k of the frame
   __syncthreads();
   // voxels of the tile, 4 per thread per iteration
   const int64_t vbase = b << kTileShift;
@@ -722,7 +767,7 @@ inline int64_t point_threads(int64_t n, int32_t rings) {
 
 cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
                            const Dims& d, uint32_t* miss_grid, uint32_t* bits,
-                           const TileCounts& tc, cudaStream_t st) {
+                           const TileCounts& tc, bool last_sensor, cudaStream_t st) {
   const int64_t threads = point_threads(n, rings);
   if (threads == 0) return cudaSuccess;
   // small blocks: a frame is one wave of warps; many small blocks spread the
@@ -732,8 +777,24 @@ cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const Se
     const int v = e ? atoi(e) : 64;
     return (v >= 32 && v <= 256 && v % 32 == 0) ? v : 64;
   }();
+  static const bool match = [] {
+    const char* e = getenv("GVOM_RAY_AGG");
+    return e && e[0] == 'm';
+  }();
   const int64_t blocks = (threads + bs - 1) / bs;
-  k_raycast<<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits, tc);
+  static const bool ddafirst = [] {
+    const char* e = getenv("GVOM_RAY_ORDER");
+    return e && e[0] == 'd';
+  }();
+  if (match)
+    k_raycast<true, true><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits,
+                                                           tc, last_sensor);
+  else if (ddafirst)
+    k_raycast<false, false><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid,
+                                                             bits, tc, last_sensor);
+  else
+    k_raycast<false, true><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits,
+                                                            tc, last_sensor);
   return cudaGetLastError();
 }
 
@@ -779,10 +840,10 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
 }
 
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
-                                  gvom_voxel* data, const TileCounts& tc, uint32_t* total,
-                                  const Dims& d, cudaStream_t st) {
+                                  gvom_voxel* data, const TileCounts& tc, const Dims& d,
+                                  cudaStream_t st) {
   k_finalize_tiles<<<(unsigned)n_tiles(d), kTileWords, 0, st>>>(lut_inplace, bits, wprefix, data,
-                                                                tc, total, d);
+                                                                tc, d);
   return cudaGetLastError();
 }
 
