@@ -126,10 +126,12 @@ __device__ __forceinline__ bool after(float k, int a, float K, int A) {
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane);
 
 // The frame's last finishing ray-cast block (of the last sensor's launch)
-// turns the tile counts into exclusive offsets and the frame's k.
+// turns the tile counts into exclusive offsets: each thread sums a
+// contiguous chunk, one block scan of the chunk sums, then each thread
+// writes its chunk's running offsets.
 __device__ void scan_tiles_if_last(const TileCounts& tc, const Dims& d) {
   __shared__ bool last;
-  __shared__ uint32_t wsum[32], carry;
+  __shared__ uint32_t wsum[32];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(tc.done, 1u) == gridDim.x - 1;
@@ -137,26 +139,24 @@ __device__ void scan_tiles_if_last(const TileCounts& tc, const Dims& d) {
   if (!last) return;
   __threadfence();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
   const int64_t nt = n_tiles(d);
-  for (int64_t base = 0; base < nt; base += blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const uint32_t v = i < nt ? __ldcg(tc.tile + i) : 0u;
-    const uint32_t inc = warp_incl_scan(v, lane);
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const uint32_t w = lane < nw ? wsum[lane] : 0u;
-      const uint32_t e = warp_incl_scan(w, lane) - w;
-      if (lane < nw) wsum[lane] = e;
-    }
-    __syncthreads();
-    const uint32_t ex = carry + wsum[wid] + inc - v;
-    if (i < nt) tc.offset[i] = ex;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = ex + v;
-    __syncthreads();
+  const int64_t chunk = (nt + blockDim.x - 1) / blockDim.x;
+  const int64_t c0 = threadIdx.x * chunk, c1 = min(nt, c0 + chunk);
+  uint32_t sum = 0;
+  for (int64_t i = c0; i < c1; ++i) sum += __ldcg(tc.tile + i);
+  const uint32_t inc = warp_incl_scan(sum, lane);
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t w = lane < nw ? wsum[lane] : 0u;
+    const uint32_t e = warp_incl_scan(w, lane) - w;
+    if (lane < nw) wsum[lane] = e;
+  }
+  __syncthreads();
+  uint32_t run = wsum[wid] + inc - sum;
+  for (int64_t i = c0; i < c1; ++i) {
+    tc.offset[i] = run;
+    run += __ldcg(tc.tile + i);
   }
 }
 

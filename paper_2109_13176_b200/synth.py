@@ -189,11 +189,12 @@ def _cast_terrain(world: World, P: torch.Tensor, D: torch.Tensor, tmax: float,
                   dt: float = 0.1, chunk: int = 48) -> torch.Tensor:
     """First t in (0, tmax] with z(t) < h(x(t), y(t)); inf if none."""
     n = D.shape[0]
-    out = torch.full((n,), math.inf, dtype=torch.float64)
+    dev = D.device
+    out = torch.full((n,), math.inf, dtype=torch.float64, device=dev)
     lo_b, hi_b = world.height_bound()
     dz = D[:, 2]
     # skip the part of each ray that is certainly above the terrain bound
-    t0 = torch.zeros(n, dtype=torch.float64)
+    t0 = torch.zeros(n, dtype=torch.float64, device=dev)
     if P[2] > hi_b:
         down = dz < 0
         t0 = torch.where(down, (hi_b - P[2]) / dz, torch.full_like(dz, math.inf))
@@ -202,7 +203,7 @@ def _cast_terrain(world: World, P: torch.Tensor, D: torch.Tensor, tmax: float,
     alive = t0 < tmax
     idx = torch.nonzero(alive).squeeze(1)
     tcur = t0[idx]
-    steps = torch.arange(1, chunk + 1, dtype=torch.float64) * dt
+    steps = torch.arange(1, chunk + 1, dtype=torch.float64, device=dev) * dt
     while idx.numel() > 0:
         Dk = D[idx]
         ts = tcur[:, None] + steps[None, :]  # [m, chunk]
@@ -254,8 +255,10 @@ def _az_interval_rays(az_sorted, order, center_az, half):
             segs.append((a, b))
     parts = []
     for a, b in segs:
-        i0 = int(torch.searchsorted(az_sorted, torch.tensor(a, dtype=torch.float64)))
-        i1 = int(torch.searchsorted(az_sorted, torch.tensor(b, dtype=torch.float64), right=True))
+        ta = torch.tensor([a], dtype=torch.float64, device=az_sorted.device)
+        tb = torch.tensor([b], dtype=torch.float64, device=az_sorted.device)
+        i0 = int(torch.searchsorted(az_sorted, ta)[0])
+        i1 = int(torch.searchsorted(az_sorted, tb, right=True)[0])
         if i1 > i0:
             parts.append(order[i0:i1])
     if not parts:
@@ -263,15 +266,26 @@ def _az_interval_rays(az_sorted, order, center_az, half):
     return torch.cat(parts)
 
 
+def default_device() -> str:
+    """Geometry device of the generator: the GPU when present (harness code;
+    results are deterministic per device).  GVOM_SYNTH_DEVICE overrides."""
+    import os
+    env = os.environ.get("GVOM_SYNTH_DEVICE")
+    if env:
+        return env
+    return "cuda" if torch.cuda.is_available() else "cpu"
+
+
 def cast_scan(world: World, lidar: Lidar, pose: np.ndarray, *, seed: int, frame: int,
-              sensor: int, noise: bool = True) -> np.ndarray:
+              sensor: int, noise: bool = True, device: Optional[str] = None) -> np.ndarray:
     """Simulate one scan; returns sensor-frame float32 points [N, 4] (w = 0)."""
-    R = torch.from_numpy(np.ascontiguousarray(pose[:, :3]))
-    P = torch.from_numpy(np.ascontiguousarray(pose[:, 3]))
-    d_s = lidar.directions()  # sensor frame
+    dev = torch.device(device or default_device())
+    R = torch.from_numpy(np.ascontiguousarray(pose[:, :3])).to(dev)
+    P = torch.from_numpy(np.ascontiguousarray(pose[:, 3])).to(dev)
+    d_s = lidar.directions().to(dev)  # sensor frame
     D = d_s @ R.T  # world
     n = D.shape[0]
-    t_best = torch.full((n,), BACKDROP_RANGE, dtype=torch.float64)
+    t_best = torch.full((n,), BACKDROP_RANGE, dtype=torch.float64, device=dev)
     # terrain
     t_best = torch.minimum(t_best, _cast_terrain(world, P, D, BACKDROP_RANGE))
     # azimuth index for culling
@@ -295,7 +309,7 @@ def cast_scan(world: World, lidar: Lidar, pose: np.ndarray, *, seed: int, frame:
         if ids.numel() == 0:
             continue
         Dk = D[ids]
-        tmin = torch.zeros(ids.numel(), dtype=torch.float64)
+        tmin = torch.zeros(ids.numel(), dtype=torch.float64, device=dev)
         tmax = t_best[ids].clone()
         for ax, (a0, a1) in enumerate(((x0, x1), (y0, y1), (z0, z1))):
             da = Dk[:, ax]
@@ -333,8 +347,8 @@ def cast_scan(world: World, lidar: Lidar, pose: np.ndarray, *, seed: int, frame:
             continue
         Dk = D[ids]
         o = torch.tensor([(float(P[0]) - cx) / rx, (float(P[1]) - cy) / ry, (float(P[2]) - cz) / rz],
-                         dtype=torch.float64)
-        dk = Dk / torch.tensor([rx, ry, rz], dtype=torch.float64)
+                         dtype=torch.float64, device=dev)
+        dk = Dk / torch.tensor([rx, ry, rz], dtype=torch.float64, device=dev)
         a = (dk * dk).sum(1)
         b = 2 * (dk * o).sum(1)
         c = float((o * o).sum()) - 1.0
@@ -354,7 +368,7 @@ def cast_scan(world: World, lidar: Lidar, pose: np.ndarray, *, seed: int, frame:
         if ids.numel() == 0:
             continue
         Dk = D[ids]
-        tmin = torch.zeros(ids.numel(), dtype=torch.float64)
+        tmin = torch.zeros(ids.numel(), dtype=torch.float64, device=dev)
         tmax = t_best[ids].clone()
         for ax, (a0, a1) in enumerate(((x0, x1), (y0, y1), (z0, z1))):
             da = Dk[:, ax]
@@ -369,13 +383,13 @@ def cast_scan(world: World, lidar: Lidar, pose: np.ndarray, *, seed: int, frame:
             continue
         _veg_terminate(ids[ok], tmin[ok], tmax[ok], p, t_best, seed, frame, sensor,
                        100000 + vid2, lidar.rings)
-    rng = t_best.numpy().copy()
+    rng = t_best.cpu().numpy().copy()
     if noise and lidar.noise_sigma > 0:
         beam = np.arange(n, dtype=np.int64)
         rng = rng + lidar.noise_sigma * normal(seed, frame, sensor, beam % lidar.rings,
                                                beam // lidar.rings, 7)
     pts = np.zeros((n, 4), dtype=np.float32)
-    pts[:, :3] = (d_s.numpy() * rng[:, None]).astype(np.float32)
+    pts[:, :3] = (d_s.cpu().numpy() * rng[:, None]).astype(np.float32)
     return pts
 
 
@@ -383,23 +397,23 @@ def _veg_terminate(ids, t0, t1, p, t_best, seed, frame, sensor, vid, rings):
     step = 0.25
     nsteps = torch.ceil((t1 - t0) / step).to(torch.int64)
     maxs = int(nsteps.max())
-    idn = ids.numpy().astype(np.int64)
+    idn = ids.cpu().numpy().astype(np.int64)
     ring = idn % rings
     col = idn // rings
     js = np.arange(maxs, dtype=np.int64)
     u = uniform(seed, frame, sensor, ring[:, None], col[:, None], vid, js[None, :], 11)
     u2 = uniform(seed, frame, sensor, ring[:, None], col[:, None], vid, js[None, :], 13)
-    valid = js[None, :] < nsteps.numpy()[:, None]
+    valid = js[None, :] < nsteps.cpu().numpy()[:, None]
     term = (u < p) & valid
     anyt = term.any(axis=1)
     if not anyt.any():
         return
     first = np.argmax(term, axis=1)
     rows = np.nonzero(anyt)[0]
-    tt = t0.numpy()[rows] + (first[rows] + u2[rows, first[rows]]) * step
-    tt = np.minimum(tt, t1.numpy()[rows])
-    tgt = torch.from_numpy(idn[rows])
-    t_best[tgt] = torch.minimum(t_best[tgt], torch.from_numpy(tt))
+    tt = t0.cpu().numpy()[rows] + (first[rows] + u2[rows, first[rows]]) * step
+    tt = np.minimum(tt, t1.cpu().numpy()[rows])
+    tgt = torch.from_numpy(idn[rows]).to(t_best.device)
+    t_best[tgt] = torch.minimum(t_best[tgt], torch.from_numpy(tt).to(t_best.device))
 
 
 # ----------------------------------------------------------------------------

@@ -158,3 +158,11 @@ def test_multi_stream_handles_independent(c2):
     la, lb = layers_np(a), layers_np(b)
     for k in la:
         assert np.array_equal(np.nan_to_num(la[k], nan=-7), np.nan_to_num(lb[k], nan=-7))
+
+
+@pytest.mark.slow
+def test_c5_large_map_full_size():
+    # BASELINE configs[4] at full size in bench.py's launch configuration:
+    # 8 streams x 524,288 points, 1024x1024x128 voxels at 0.1 m, K = 1.
+    # The oracle runs the whole frame (~30 s single-threaded C).
+    run_sequence(synth.workload(4), check_merged=False)
