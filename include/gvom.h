@@ -40,6 +40,7 @@ extern "C" {
 #define GVOM_ABI_VERSION 1
 #define GVOM_MAX_BUFFER_FRAMES 32
 #define GVOM_MAX_SENSORS 64
+#define GVOM_MAX_RANKS 64
 
 typedef enum gvom_status {
   GVOM_OK = 0,
@@ -179,6 +180,41 @@ GVOM_API gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_vox
  * produced by integrate_scan.  Synchronous.                               */
 GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_voxel* d_data,
                               int64_t cap, int64_t* out_k, int64_t out_origin[3]);
+
+/* ---- Multi-GPU slab partition -----------------------------
+ * The points of one frame are sharded across P ranks (one process and handle
+ * per GPU, buffer_frames must be 1); rank r owns the y-rows
+ * [slab_y[r], slab_y[r+1]), which in L order is the contiguous voxel range
+ * [slab_y[r]*nx*nz, slab_y[r+1]*nx*nz).  Per frame, with the collectives done
+ * by the caller (torch.distributed / NCCL; paper_2109_13176_b200/parallel.py):
+ *  1. gvom_partial_scan on the rank's sensors: a dense u32 miss grid [V] and
+ *     the in-grid returns as gvom_endpoint records grouped by destination slab;
+ *  2. reduce-scatter (SUM) of the miss grids by slab; all-to-all of records;
+ *  3. gvom_slab_occupancy -> k of the slab; all-gather of k -> rank base;
+ *  4. gvom_slab_finalize: LUT + data rows of the slab (local ranks; global
+ *     rank = base + local), pushed into the buffer;
+ *  5. gvom_compute_maps_slab(phase 0): columns of the slab rows; all-gather of
+ *     the q_s rows into gvom_surface_buffer(); phase 1: slope, roughness and
+ *     negative obstacles for the whole map from the gathered surface.
+ * Sums and mins are exact integers, so the result is identical to one GPU.  */
+typedef struct gvom_endpoint {
+  uint32_t L;  /* linear voxel index of an in-grid return          */
+  uint32_t dz; /* fixed-point height above the voxel floor (A12)   */
+} gvom_endpoint;
+
+GVOM_API gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                       uint32_t* d_miss, gvom_endpoint* d_ep, int64_t ep_cap,
+                                       const int32_t* slab_y, int32_t n_ranks,
+                                       int64_t* out_counts);
+GVOM_API gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1,
+                                         const gvom_endpoint* d_ep, int64_t n_ep, int64_t* out_k);
+GVOM_API gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
+                                        const uint32_t* d_miss_slab, const gvom_endpoint* d_ep,
+                                        int64_t n_ep);
+GVOM_API gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1,
+                                            int32_t phase);
+/* device pointer of the [ny][nx] int32 surface buffer (q_s, INT32_MIN = none) */
+GVOM_API gvom_status gvom_surface_buffer(gvom_handle* h, int32_t** out_d_qs);
 
 /* Instrumentation.  gvom_set_timing(h, mask): every launch of a stage whose
  * bit (1 << GVOM_STAGE_*) is set in mask is bracketed by CUDA events on the

@@ -31,7 +31,7 @@ struct Slot {
 
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
-  size_t staging, rank_tmp, rank_status, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
+  size_t staging, rank_tmp, rank_status, epcnt, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
       total;
   int64_t cap, nblk, cells;
 };
@@ -83,6 +83,8 @@ Layout make_layout(const gvom_config* c) {
   off += align_up(4 * (size_t)(l.nblk + 2));
   l.rank_status = off;  // [0] ticket counter, [1 + b] tile status (decoupled look-back)
   off += align_up(8 * (size_t)(l.nblk + 1));
+  l.epcnt = off;  // slab partition: per-destination record counts and cursors
+  off += align_up(4 * 2 * (size_t)GVOM_MAX_RANKS);
   l.tilecnt = off;  // per finalize tile: occupancy counts, offsets; then the done counter
   l.tilecnt_bytes = align_up(4 * (size_t)(2 * n_tiles(d) + 4));
   off += l.tilecnt_bytes;
@@ -135,6 +137,8 @@ struct gvom_handle {
   uint64_t rank_calls = 0;  // decoupled look-back epochs / ticket base
   uint32_t timing_mask = 0;  // stages bracketed by CUDA events
   TileCounts tc{};
+  // slab partition: occupancy built by gvom_slab_occupancy, pending finalize
+  int32_t slab_y0 = -1, slab_y1 = -1;
 };
 
 namespace {
@@ -378,10 +382,11 @@ gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_
   return GVOM_OK;
 }
 
-gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
+// Validate a frame's scans and fold their poses (A4); sensor voxels in grid (A9).
+static gvom_status prepare_scans(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                 SensorParams* sp) {
   if (!h || n_scans < 0 || n_scans > GVOM_MAX_SENSORS || (n_scans > 0 && !scans))
     return GVOM_E_INVALID;
-  SensorParams sp[GVOM_MAX_SENSORS];
   int64_t total = 0;
   for (int i = 0; i < n_scans; ++i) {
     const gvom_scan& s = scans[i];
@@ -399,6 +404,35 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
         !isfinite(p.b[2]))
       return GVOM_E_SENSOR_OUTSIDE;
   }
+  return GVOM_OK;
+}
+
+// Device pointers of the scans' points (host points are staged, stream-ordered).
+static gvom_status stage_points(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                std::vector<const float4*>& dptr) {
+  dptr.assign(n_scans, nullptr);
+  int64_t off = 0;
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n == 0) continue;
+    if (is_device_ptr(s.xyzw)) {
+      dptr[i] = (const float4*)s.xyzw;
+    } else {
+      float4* dst = h->staging + off;
+      GVOM_CU(stage(h, GVOM_STAGE_H2D, false, [&] {
+        return cudaMemcpyAsync(dst, s.xyzw, 16 * (size_t)s.n, cudaMemcpyHostToDevice, h->st);
+      }));
+      dptr[i] = dst;
+      off += s.n;
+    }
+  }
+  return GVOM_OK;
+}
+
+gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
+  SensorParams sp[GVOM_MAX_SENSORS];
+  const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
+  if (ps != GVOM_OK) return ps;
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
@@ -412,24 +446,14 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   int last_scan = -1;
   for (int i = 0; i < n_scans; ++i)
     if (scans[i].n > 0) last_scan = i;
-  std::vector<const float4*> dptr(n_scans);
-  int64_t off = 0;
+  std::vector<const float4*> dptr;
+  {
+    const gvom_status st = stage_points(h, scans, n_scans, dptr);
+    if (st != GVOM_OK) return st;
+  }
   for (int i = 0; i < n_scans; ++i) {
     const gvom_scan& s = scans[i];
-    if (s.n == 0) {
-      dptr[i] = nullptr;
-      continue;
-    }
-    if (is_device_ptr(s.xyzw)) {
-      dptr[i] = (const float4*)s.xyzw;
-    } else {
-      float4* dst = h->staging + off;
-      GVOM_CU(stage(h, GVOM_STAGE_H2D, false, [&] {
-        return cudaMemcpyAsync(dst, s.xyzw, 16 * (size_t)s.n, cudaMemcpyHostToDevice, h->st);
-      }));
-      dptr[i] = dst;
-      off += s.n;
-    }
+    if (s.n == 0) continue;
     GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
       return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits, tc,
                             i == last_scan, h->st);
@@ -577,6 +601,163 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
     GVOM_CU(cudaMemcpyAsync(d_data, s.data, sizeof(gvom_voxel) * (size_t)k, cudaMemcpyDefault,
                             h->st));
   GVOM_CU(cudaStreamSynchronize(h->st));
+  return GVOM_OK;
+}
+
+// ---- multi-GPU slab partition --------------------------------
+static bool slab_ok(const gvom_handle* h, int32_t y0, int32_t y1) {
+  return h && h->cfg.buffer_frames == 1 && y0 >= 0 && y1 <= h->cfg.ny && y0 < y1;
+}
+
+gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                              uint32_t* d_miss, gvom_endpoint* d_ep, int64_t ep_cap,
+                              const int32_t* slab_y, int32_t n_ranks, int64_t* out_counts) {
+  if (!h || !d_miss || !slab_y || !out_counts || n_ranks < 1 || n_ranks > GVOM_MAX_RANKS ||
+      ep_cap < 0 || (ep_cap > 0 && !d_ep))
+    return GVOM_E_INVALID;
+  SlabBounds sb;
+  sb.P = n_ranks;
+  for (int r = 0; r <= n_ranks; ++r) sb.y[r] = slab_y[r];
+  if (sb.y[0] != 0 || sb.y[n_ranks] != h->cfg.ny) return GVOM_E_INVALID;
+  for (int r = 0; r < n_ranks; ++r)
+    if (sb.y[r + 1] < sb.y[r]) return GVOM_E_INVALID;
+  SensorParams sp[GVOM_MAX_SENSORS];
+  const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
+  if (ps != GVOM_OK) return ps;
+  std::vector<const float4*> dptr;
+  {
+    const gvom_status st = stage_points(h, scans, n_scans, dptr);
+    if (st != GVOM_OK) return st;
+  }
+  const Dims& d = h->d;
+  uint32_t* cnt = (uint32_t*)(h->ws + h->lay.epcnt);
+  uint32_t* cur = cnt + GVOM_MAX_RANKS;
+  GVOM_CU(cudaMemsetAsync(d_miss, 0, 4 * (size_t)d.V, h->st));
+  GVOM_CU(cudaMemsetAsync(cnt, 0, 4 * (size_t)GVOM_MAX_RANKS, h->st));
+  TileCounts none{};
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n == 0) continue;
+    GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
+      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, d_miss, nullptr, none, false, h->st);
+    }));
+    GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true,
+                  [&] { return launch_ep_count(dptr[i], s.n, sp[i], d, sb, cnt, h->st); }));
+  }
+  uint32_t hc[GVOM_MAX_RANKS];
+  GVOM_CU(cudaMemcpyAsync(hc, cnt, 4 * (size_t)n_ranks, cudaMemcpyDeviceToHost, h->st));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  uint32_t ho[GVOM_MAX_RANKS];
+  int64_t tot = 0;
+  for (int r = 0; r < n_ranks; ++r) {
+    ho[r] = (uint32_t)tot;
+    tot += hc[r];
+    out_counts[r] = hc[r];
+  }
+  if (tot > ep_cap) return GVOM_E_SIZE;
+  GVOM_CU(cudaMemcpyAsync(cur, ho, 4 * (size_t)n_ranks, cudaMemcpyHostToDevice, h->st));
+  for (int i = 0; i < n_scans; ++i) {
+    const gvom_scan& s = scans[i];
+    if (s.n == 0) continue;
+    GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
+      return launch_ep_write(dptr[i], s.n, sp[i], d, sb, cur, (EpRecord*)d_ep, h->st);
+    }));
+  }
+  GVOM_CU(cudaStreamSynchronize(h->st));  // the host buffer ho must outlive the copy
+  return GVOM_OK;
+}
+
+static void slab_tiles(const gvom_handle* h, int32_t y0, int32_t y1, int64_t* t0, int64_t* t1) {
+  const int64_t row = (int64_t)h->cfg.nx * h->cfg.nz;
+  *t0 = (y0 * row) >> kTileShift;
+  *t1 = ((y1 * row) + (1 << kTileShift) - 1) >> kTileShift;
+}
+
+gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1, const gvom_endpoint* d_ep,
+                                int64_t n_ep, int64_t* out_k) {
+  if (!slab_ok(h, y0, y1) || !out_k || n_ep < 0 || (n_ep > 0 && !d_ep)) return GVOM_E_INVALID;
+  Slot& slot = h->slots[h->head];
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
+    return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
+                        (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
+                        h->lay.tilecnt_bytes, h->st);
+  }));
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_COUNT, true, [&] {
+    return launch_slab_bits((const EpRecord*)d_ep, n_ep, slot.bits, h->tc.tile, h->st);
+  }));
+  int64_t t0, t1;
+  slab_tiles(h, y0, y1, &t0, &t1);
+  TileCounts tc = h->tc;
+  tc.total = slot.meta;
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_SCAN, true, [&] { return launch_tile_scan(tc, t0, t1, h->st); }));
+  uint32_t k = 0;
+  GVOM_CU(cudaMemcpyAsync(&k, slot.meta, 4, cudaMemcpyDeviceToHost, h->st));
+  GVOM_CU(cudaStreamSynchronize(h->st));
+  *out_k = k;
+  h->slab_y0 = y0;
+  h->slab_y1 = y1;
+  return GVOM_OK;
+}
+
+gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uint32_t* d_miss_slab,
+                               const gvom_endpoint* d_ep, int64_t n_ep) {
+  if (!slab_ok(h, y0, y1) || !d_miss_slab || n_ep < 0 || (n_ep > 0 && !d_ep))
+    return GVOM_E_INVALID;
+  if (h->slab_y0 != y0 || h->slab_y1 != y1) return GVOM_E_INVALID;  // occupancy first
+  Slot& slot = h->slots[h->head];
+  const Dims& d = h->d;
+  const int64_t row = (int64_t)h->cfg.nx * h->cfg.nz;
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+    return cudaMemcpyAsync(slot.lut + y0 * row, d_miss_slab, 4 * (size_t)((y1 - y0) * row),
+                           cudaMemcpyDeviceToDevice, h->st);
+  }));
+  int64_t t0, t1;
+  slab_tiles(h, y0, y1, &t0, &t1);
+  TileCounts tc = h->tc;
+  tc.total = slot.meta;
+  GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
+    return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st, t0,
+                                 t1);
+  }));
+  GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
+    return launch_endpoint_records((const EpRecord*)d_ep, n_ep, slot.lut, slot.data, h->st);
+  }));
+  for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
+  h->head = (h->head + 1) % h->K;
+  if (h->count < h->K) h->count++;
+  h->slab_y0 = h->slab_y1 = -1;
+  return GVOM_OK;
+}
+
+gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32_t phase) {
+  if (!slab_ok(h, y0, y1) || (phase != 0 && phase != 1)) return GVOM_E_INVALID;
+  if (h->count == 0) return GVOM_E_EMPTY;
+  if (phase == 0) {
+    const int newest = (h->head - 1 + h->K) % h->K;
+    int64_t o[3];
+    for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
+    h->map_slots = buffer_slots(h, o);
+    h->lp.o_z = o[2];
+    GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
+      return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st, (int64_t)y0 * h->cfg.nx,
+                            (int64_t)y1 * h->cfg.nx);
+    }));
+    for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
+    return GVOM_OK;
+  }
+  GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
+                [&] { return launch_transpose_init(h->d, h->layers, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
+                [&] { return launch_negative(h->d, h->lp, h->layers, h->st); }));
+  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
+                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
+  h->maps_valid = true;
+  return GVOM_OK;
+}
+
+gvom_status gvom_surface_buffer(gvom_handle* h, int32_t** out_d_qs) {
+  if (!h || !out_d_qs) return GVOM_E_INVALID;
+  *out_d_qs = h->layers.qs;
   return GVOM_OK;
 }
 

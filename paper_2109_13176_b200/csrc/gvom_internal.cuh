@@ -85,7 +85,7 @@ cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const Se
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
-                                  cudaStream_t st);
+                                  cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1);
 cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
                               cudaStream_t st);
 cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
@@ -103,7 +103,28 @@ cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const ui
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
                             const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st);
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
-                           const LayerPtrs& out, cudaStream_t st);
+                           const LayerPtrs& out, cudaStream_t st, int64_t cbeg = 0,
+                           int64_t cend = -1);
+// ---- multi-GPU slab partition (k_slab.cu) ----
+struct SlabBounds {
+  int32_t P;
+  int32_t y[GVOM_MAX_RANKS + 1];  // slab r = rows [y[r], y[r+1])
+};
+struct EpRecord {  // == gvom_endpoint
+  uint32_t L, dz;
+};
+cudaError_t launch_ep_count(const float4* pts, int64_t n, const SensorParams& sp, const Dims& d,
+                            const SlabBounds& sb, uint32_t* counts, cudaStream_t st);
+cudaError_t launch_ep_write(const float4* pts, int64_t n, const SensorParams& sp, const Dims& d,
+                            const SlabBounds& sb, uint32_t* cursor, EpRecord* out,
+                            cudaStream_t st);
+cudaError_t launch_slab_bits(const EpRecord* ep, int64_t n, uint32_t* bits, uint32_t* tile_counts,
+                             cudaStream_t st);
+cudaError_t launch_tile_scan(const TileCounts& tc, int64_t t_begin, int64_t t_end,
+                             cudaStream_t st);
+cudaError_t launch_endpoint_records(const EpRecord* ep, int64_t n, const int32_t* lut,
+                                    gvom_voxel* data, cudaStream_t st);
+cudaError_t launch_transpose_init(const Dims& d, const LayerPtrs& out, cudaStream_t st);
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st);
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,

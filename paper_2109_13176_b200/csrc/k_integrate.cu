@@ -229,8 +229,9 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
           fin = fin && isfinite(inv[a]);
         }
       }
-      // endpoint occupancy (O4/O6: occupied iff hits >= 1)
-      if ((unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
+      // endpoint occupancy (O4/O6: occupied iff hits >= 1); bits == nullptr in
+      // the multi-GPU partial pass (occupancy is built on the slab owner)
+      if (bits && (unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
           (unsigned)E[2] < (unsigned)d.nz) {
         const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
         const uint32_t bit = 1u << (LE & 31);
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts,
     if (!kAggFirst) aggregate_red<kMatchAgg>(miss, Lc, active, act, after_lanes, lane);
     act = __ballot_sync(0xffffffffu, left > 0);
   }
-  if (last_sensor) scan_tiles_if_last(tc, d);
+  if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
@@ -621,10 +622,10 @@ __global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na
 // 8192 voxels with 16-byte accesses.
 __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
-    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d) {
+    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t_begin) {
   __shared__ uint32_t sbits[kTileWords], spre[kTileWords], wsum[kTileWords / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int64_t b = blockIdx.x;
+  const int64_t b = t_begin + blockIdx.x;
   const uint32_t off = __ldg(tc.offset + b);  // rank offset of this tile
   // per-word exclusive prefix within the tile
   const int64_t w = b * kTileWords + t;
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
   sbits[t] = bw;
   spre[t] = pre;
   if (w < d.W) wprefix[w] = pre;
-  if (b == gridDim.x - 1 && t == kTileWords - 1) *tc.total = pre + c;  // k of the frame
+  if (blockIdx.x == gridDim.x - 1 && t == kTileWords - 1) *tc.total = pre + c;  // k of the frame
   __syncthreads();
   // voxels of the tile, 4 per thread per iteration
   const int64_t vbase = b << kTileShift;
@@ -841,9 +842,11 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
 
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
-                                  cudaStream_t st) {
-  k_finalize_tiles<<<(unsigned)n_tiles(d), kTileWords, 0, st>>>(lut_inplace, bits, wprefix, data,
-                                                                tc, d);
+                                  cudaStream_t st, int64_t t_begin, int64_t t_end) {
+  if (t_end < 0) t_end = n_tiles(d);
+  if (t_end <= t_begin) return cudaSuccess;
+  k_finalize_tiles<<<(unsigned)(t_end - t_begin), kTileWords, 0, st>>>(lut_inplace, bits, wprefix,
+                                                                       data, tc, d, t_begin);
   return cudaGetLastError();
 }
 

@@ -89,13 +89,13 @@ __device__ __forceinline__ SlotVox slot_vox(bool col, const int32_t* __restrict_
 //          cross-lane traffic; only the two edge voxels need the merged
 //          min_dz (a group min).  One group sum at the end.
 __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
-                                                 const LayerParams lp, const LayerPtrs out) {
+                                                 const LayerParams lp, const LayerPtrs out,
+                                                 int64_t cbeg, int64_t cells) {
   const int lane = threadIdx.x & 31;
   const int lg = ss.kp_log2;
   const int k = lane & ((1 << lg) - 1);
-  const int64_t cells = (int64_t)d.nx * d.ny;
-  const int64_t c0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - lg);
-  if (c0 >= cells) return;  // whole warp past the end
+  const int64_t c0 = cbeg + ((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - lg));
+  if (c0 >= cells) return;  // whole warp past the end (cells = end of the range)
   const int64_t c = c0 + (lane >> lg);
   const bool cvalid = c < cells;
   const int x = cvalid ? (int)(c % d.nx) : 0, y = cvalid ? (int)(c / d.nx) : 0;
@@ -569,9 +569,11 @@ inline unsigned cells_blocks(const Dims& d, int tpb) {
 }  // namespace
 
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
-                           const LayerPtrs& out, cudaStream_t st) {
-  const int64_t lanes = ((int64_t)d.nx * d.ny) << ss.kp_log2;
-  k_columns<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out);
+                           const LayerPtrs& out, cudaStream_t st, int64_t cbeg, int64_t cend) {
+  if (cend < 0) cend = (int64_t)d.nx * d.ny;
+  if (cend <= cbeg) return cudaSuccess;
+  const int64_t lanes = (cend - cbeg) << ss.kp_log2;
+  k_columns<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend);
   return cudaGetLastError();
 }
 

@@ -96,6 +96,11 @@ def load_library() -> C.CDLL:
         "gvom_stage_times": ([P, P, I32], I32),
         "gvom_launch_count": ([P], I64),
         "gvom_status_string": ([I32], C.c_char_p),
+        "gvom_partial_scan": ([P, P, I32, P, P, I64, P, I32, P], I32),
+        "gvom_slab_occupancy": ([P, I32, I32, P, I64, P], I32),
+        "gvom_slab_finalize": ([P, I32, I32, P, P, I64], I32),
+        "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
+        "gvom_surface_buffer": ([P, P], I32),
         "gvom_abi_version": ([], I32),
     }
     for name, (args, res) in sig.items():
@@ -110,7 +115,8 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_synchronize", "gvom_shift", "gvom_integrate_scan", "gvom_compute_maps",
             "gvom_export_2d", "gvom_export_layers", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
-            "gvom_abi_version")
+            "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
+            "gvom_compute_maps_slab", "gvom_surface_buffer")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -197,6 +203,64 @@ class GvomMap:
         d = (C.c_int64 * 3)()
         _check(self.lib.gvom_shift(self.h, p, d), "gvom_shift")
         return np.array(d[:], dtype=np.int64)
+
+    def _scan_array(self, scans: Iterable[ScanLike]):
+        items = list(scans)
+        arr = (Scan * max(1, len(items)))()
+        keep = []
+        for i, it in enumerate(items):
+            pts, pose = it[0], it[1]
+            rings = int(it[2]) if len(it) > 2 else 0
+            if isinstance(pts, np.ndarray):
+                pts = torch.from_numpy(np.ascontiguousarray(pts, dtype=np.float32))
+            if pts.dtype != torch.float32 or pts.dim() != 2 or pts.shape[1] != 4:
+                raise ValueError("points must be float32 [n, 4]")
+            pts = pts.contiguous()
+            keep.append(pts)
+            arr[i].xyzw = pts.data_ptr() if pts.numel() else None
+            arr[i].n = pts.shape[0]
+            P = np.ascontiguousarray(np.asarray(pose, dtype=np.float64).reshape(12))
+            for j in range(12):
+                arr[i].sensor_to_world[j] = float(P[j])
+            arr[i].rings = rings
+        return arr, len(items), keep
+
+    # -- multi-GPU slab partition (include/gvom.h) --------------
+    def partial_scan(self, scans, miss: torch.Tensor, records: torch.Tensor, slab_y) -> list:
+        """Trace this rank's rays into `miss` (int32 [V], zeroed by the call) and
+        write its in-grid returns into `records` (int64 [cap], one 8-byte
+        gvom_endpoint each) grouped by destination slab; returns the counts."""
+        arr, n, keep = self._scan_array(scans)
+        P = len(slab_y) - 1
+        ys = (C.c_int32 * (P + 1))(*[int(v) for v in slab_y])
+        cnt = (C.c_int64 * P)()
+        _check(self.lib.gvom_partial_scan(self.h, arr, n, C.c_void_p(miss.data_ptr()),
+                                          C.c_void_p(records.data_ptr()), records.numel(), ys, P,
+                                          cnt), "gvom_partial_scan")
+        return [int(c) for c in cnt]
+
+    def slab_occupancy(self, y0: int, y1: int, records: torch.Tensor, n: int) -> int:
+        k = C.c_int64()
+        _check(self.lib.gvom_slab_occupancy(self.h, y0, y1, C.c_void_p(records.data_ptr()), n,
+                                            C.byref(k)), "gvom_slab_occupancy")
+        return k.value
+
+    def slab_finalize(self, y0: int, y1: int, miss_slab: torch.Tensor, records: torch.Tensor,
+                      n: int):
+        _check(self.lib.gvom_slab_finalize(self.h, y0, y1, C.c_void_p(miss_slab.data_ptr()),
+                                           C.c_void_p(records.data_ptr()), n),
+               "gvom_slab_finalize")
+
+    def compute_maps_slab(self, y0: int, y1: int, phase: int):
+        _check(self.lib.gvom_compute_maps_slab(self.h, y0, y1, phase), "gvom_compute_maps_slab")
+
+    def surface(self) -> torch.Tensor:
+        """int32 [ny, nx] view of the library's surface buffer (q_s; INT32_MIN = none)."""
+        ptr = C.c_void_p()
+        _check(self.lib.gvom_surface_buffer(self.h, C.byref(ptr)), "gvom_surface_buffer")
+        off = ptr.value - self.workspace.data_ptr()
+        n = self.nx * self.ny * 4
+        return self.workspace[off:off + n].view(torch.int32).view(self.ny, self.nx)
 
     def integrate_scan(self, scans: Iterable[ScanLike]):
         """scans: (points, pose[3,4], rings).  points: float32 [n,4] torch tensor

@@ -1,0 +1,104 @@
+"""Multi-GPU slab partition of one frame, collectives only.
+
+One process per GPU (torch.distributed, NCCL over NVLink; gloo on CPU for the
+tests).  Rank r of P owns the y-rows [y_r, y_{r+1}) of the map; in L order
+(z + nz*(x + nx*y)) that is one contiguous voxel range, so the exchange is:
+
+  miss grids   -> reduce_scatter_tensor(SUM): integer sums, exact  ("hits
+                  and misses being added together")
+  returns      -> all_to_all_single of 8-byte (L, dz) records to the slab owner
+  slab k       -> all_gather: global rank of a slab's voxel = sum of the k of the
+                  slabs before it + its local rank (ranks stay in L order)
+  surface rows -> all_gather_into_tensor of q_s rows (slope / cone-search halos)
+
+The compute steps are the C-ABI slab calls (gvom_partial_scan,
+gvom_slab_occupancy, gvom_slab_finalize, gvom_compute_maps_slab).  Because
+every reduction is an exact integer sum or min, the result is identical to the
+single-GPU map; tests/test_multi_rank_cpu.py checks the exchange with gloo and
+the oracle, tests/test_gpu_slab.py checks the kernels with P emulated ranks.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def slab_rows(ny: int, P: int) -> List[int]:
+    """Equal y-slabs (reduce_scatter_tensor needs equal chunks)."""
+    if ny % P:
+        raise ValueError(f"ny={ny} is not divisible by {P} ranks")
+    return [r * (ny // P) for r in range(P + 1)]
+
+
+def exchange_misses(miss_full: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the ranks' dense miss grids and keep this rank's slab (int32 [V/P])."""
+    P = dist.get_world_size(group)
+    out = torch.empty(miss_full.numel() // P, dtype=miss_full.dtype, device=miss_full.device)
+    dist.reduce_scatter_tensor(out, miss_full, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def route_records(records: torch.Tensor, send_counts: Sequence[int], group=None) -> torch.Tensor:
+    """all-to-all of the (L, dz) records (int64 each), grouped by destination."""
+    dev = records.device
+    sc = torch.tensor(list(send_counts), dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    rcl = [int(v) for v in rc.tolist()]
+    total = int(sum(send_counts))
+    out = torch.empty(max(sum(rcl), 1), dtype=records.dtype, device=dev)
+    dist.all_to_all_single(out[:sum(rcl)], records[:total].contiguous(),
+                           output_split_sizes=rcl, input_split_sizes=list(send_counts),
+                           group=group)
+    return out[:sum(rcl)]
+
+
+def rank_base(k_local: int, device, group=None) -> Tuple[int, int, List[int]]:
+    """(global rank of this slab's first occupied voxel, total k, all k)."""
+    P = dist.get_world_size(group)
+    t = torch.tensor([k_local], dtype=torch.int64, device=device)
+    allk = torch.empty(P, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(allk, t, group=group)
+    ks = [int(v) for v in allk.tolist()]
+    r = dist.get_rank(group)
+    return sum(ks[:r]), sum(ks), ks
+
+
+def gather_rows(full: torch.Tensor, y0: int, y1: int, group=None):
+    """all-gather equal row slabs of a [ny, ...] tensor in place."""
+    mine = full[y0:y1].contiguous().clone()
+    dist.all_gather_into_tensor(full.view(-1), mine.view(-1), group=group)
+
+
+class SlabMapper:
+    """Drives one rank's GvomMap (buffer_frames = 1) through a distributed frame."""
+
+    def __init__(self, m, group=None, ep_capacity: Optional[int] = None):
+        self.m = m
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.ys = slab_rows(m.ny, self.P)
+        self.y0, self.y1 = self.ys[self.rank], self.ys[self.rank + 1]
+        V = m.nx * m.ny * m.nz
+        dev = m.device
+        self.miss = torch.empty(V, dtype=torch.int32, device=dev)
+        cap = ep_capacity or int(m.cfg.max_points_per_frame)
+        self.records = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        self.base = 0
+        self.k_total = 0
+
+    def integrate(self, scans_local):
+        counts = self.m.partial_scan(scans_local, self.miss, self.records, self.ys)
+        miss_slab = exchange_misses(self.miss, self.group)
+        recv = route_records(self.records, counts, self.group)
+        k = self.m.slab_occupancy(self.y0, self.y1, recv, recv.numel())
+        self.base, self.k_total, _ = rank_base(k, self.m.device, self.group)
+        self.m.slab_finalize(self.y0, self.y1, miss_slab, recv, recv.numel())
+
+    def compute_maps(self):
+        self.m.compute_maps_slab(self.y0, self.y1, 0)
+        gather_rows(self.m.surface(), self.y0, self.y1, self.group)
+        self.m.compute_maps_slab(self.y0, self.y1, 1)

@@ -1,0 +1,149 @@
+"""Multi-rank (world size 2, gloo, CPU) test of the slab partition's exchange
+(paper_2109_13176_b200/parallel.py).
+
+Each rank owns one sensor of a two-lidar frame.  The compute steps are played
+by the oracle (dense miss grid and (L, dz) return records of its own sensor);
+the exchange is the product's code: reduce-scatter of the miss grids by
+y-slab, all-to-all routing of the records to the slab owner, all-gather of the
+slab occupancy counts into global rank offsets, all-gather of surface rows.
+Each rank then encodes its slab and checks it against the single-process
+oracle frame of both sensors: LUT (ranks shifted by the slab's base), data
+rows and surface rows must be identical -- the partition algebra is exact.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _frame():
+    from paper_2109_13176_b200 import synth
+    w = synth.config1(noise=True)
+    lid = synth.Lidar(16, 400, (-40.0, 15.0))
+    pose_b = synth.pose_matrix(synth.rot_zyx(0.7), (1.5, -1.0, 0.8))
+    pts_b = synth.cast_scan(w.world, lid, pose_b, seed=5, frame=0, sensor=1, device="cpu")
+    s_a = w.frames[0].scans[0]
+    return w.grid, [(s_a.points, s_a.pose), (pts_b, pose_b)]
+
+
+def _records(om_dims, res, origin, pts, pose):
+    """(L, dz) of the in-grid returns, computed with the oracle's O3/O4 steps."""
+    from oracle import oracle as O
+    nx, ny, nz = om_dims
+    A, b = O.affine(pose, res, origin)
+    recs = []
+    for p in pts:
+        ok, g = O.transform_point(A, b, *p[:3])
+        if not ok:
+            continue
+        v = np.floor(g.astype(np.float64)).astype(np.int64)
+        if np.all(v >= 0) and np.all(v < np.array([nx, ny, nz])):
+            qz = int(np.floor(np.float32(g[2]) * np.float32(65536)))
+            dz = qz - 65536 * int(v[2])
+            L = int(v[2] + nz * (v[0] + nx * v[1]))
+            recs.append((L, dz, int(v[1])))
+    return recs
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import sys
+        sys.path.insert(0, ROOT)
+        from oracle import oracle as O
+        from paper_2109_13176_b200 import parallel
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        grid, scans = _frame()
+        dims = (grid["nx"], grid["ny"], grid["nz"])
+        nx, ny, nz = dims
+        V = nx * ny * nz
+        res = grid["res"]
+        origin = O.snap_origin(nx, ny, nz, res, 0.5, (0.0, 0.0, 0.0))
+        ys = parallel.slab_rows(ny, world)
+        y0, y1 = ys[rank], ys[rank + 1]
+        # --- this rank's compute (oracle stands in for gvom_partial_scan) ---
+        pts, pose = scans[rank]
+        h, m, mn, m1, m2, st = O.integrate_dense(dims, [(pts, pose)], res, origin)
+        recs = _records(dims, res, origin, pts, pose)
+        by_dest = [[(L, dz) for (L, dz, y) in recs if ys[r] <= y < ys[r + 1]] for r in range(world)]
+        counts = [len(b) for b in by_dest]
+        flat = [L | (dz << 32) for b in by_dest for (L, dz) in b]
+        records = torch.tensor(flat + [0], dtype=torch.int64)
+        miss = torch.from_numpy(m.astype(np.int32))
+        # --- the product's exchange ---
+        miss_slab = parallel.exchange_misses(miss)
+        recv = parallel.route_records(records, counts)
+        # slab owner: occupancy + stats from the routed records (oracle O4/O6)
+        L = (recv & 0xFFFFFFFF).numpy().astype(np.int64)
+        dz = (recv >> 32).numpy().astype(np.int64)
+        v0, v1 = y0 * nx * nz, y1 * nx * nz
+        assert np.all((L >= v0) & (L < v1))
+        sl = L - v0
+        n = v1 - v0
+        hits = np.bincount(sl, minlength=n).astype(np.uint32)
+        mind = np.full(n, 0xFFFFFFFF, np.uint32)
+        np.minimum.at(mind, sl, dz.astype(np.uint32))
+        mm1 = np.zeros(n, np.uint64)
+        np.add.at(mm1, sl, dz.astype(np.uint64))
+        mm2 = np.zeros(n, np.uint64)
+        np.add.at(mm2, sl, (dz * dz).astype(np.uint64))
+        fm = O.frame_map(hits, miss_slab.numpy().astype(np.uint32), mind, mm1, mm2, origin)
+        base, k_total, ks = parallel.rank_base(fm.k, "cpu")
+        # --- reference: both sensors in one oracle frame -----------------
+        H, M, MN, M1, M2, _ = O.integrate_dense(dims, scans, res, origin)
+        ref = O.frame_map(H, M, MN, M1, M2, origin)
+        assert k_total == ref.k
+        lut_ref = ref.lut[v0:v1].astype(np.int64)
+        lut_got = fm.lut.astype(np.int64)
+        lut_got = np.where(lut_got >= 0, lut_got + base, lut_got)
+        assert np.array_equal(lut_got, lut_ref)
+        for f in ("hits", "misses", "min_dz", "m1", "m2"):
+            assert np.array_equal(getattr(fm, f), getattr(ref, f)[base:base + fm.k]), f
+        # --- surface rows: columns of the slab, then all-gather ------------
+        T = O.thresholds(res, grid["min_obstacle_height"], grid["max_obstacle_height"],
+                         grid["density_threshold"], grid["neg_obs_threshold"])
+        Hs, Mis, mns, _, _ = O.combine((nx, y1 - y0, nz), [fm], origin)
+        _, _, _, _, qs_slab, dfn_slab = O.columns((nx, y1 - y0, nz), res, origin[2], T, Hs, Mis,
+                                                  mns)
+        qs_full = torch.zeros((ny, nx), dtype=torch.int32)
+        qs_full[y0:y1] = torch.from_numpy(np.where(dfn_slab == 1, qs_slab, np.int32(-2 ** 31)))
+        parallel.gather_rows(qs_full, y0, y1)
+        Hr, Mir, mnr, _, _ = O.combine(dims, [ref], origin)
+        _, _, _, _, qs_r, dfn_r = O.columns(dims, res, origin[2], T, Hr, Mir, mnr)
+        want = np.where(dfn_r == 1, qs_r, np.int32(-2 ** 31))
+        assert np.array_equal(qs_full.numpy(), want)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok", fm.k, base))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "fail", traceback.format_exc(), None))
+
+
+def test_slab_exchange_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 200)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info, base in res:
+        assert status == "ok", info
+    bases = sorted((r[0], r[3]) for r in res)
+    assert bases[0][1] == 0
+
+
+def test_slab_rows():
+    from paper_2109_13176_b200 import parallel
+    assert parallel.slab_rows(1024, 8) == [0, 128, 256, 384, 512, 640, 768, 896, 1024]
+    with pytest.raises(ValueError):
+        parallel.slab_rows(100, 8)
