@@ -139,6 +139,9 @@ struct gvom_handle {
   TileCounts tc{};
   // slab partition: occupancy built by gvom_slab_occupancy, pending finalize
   int32_t slab_y0 = -1, slab_y1 = -1;
+  // fork/join: the cone search runs on `aux` while k_slope runs on `st`
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -156,17 +159,18 @@ cudaEvent_t take_event(gvom_handle* h) {
 
 // Run one stage (a kernel launch or a copy) with optional event timing.
 template <class F>
-cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f) {
+cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f, cudaStream_t on = nullptr) {
   cudaEvent_t a = nullptr, b = nullptr;
   const bool timed = h->timing && ((h->timing_mask >> id) & 1u);
+  cudaStream_t ts = on ? on : h->st;
   if (timed) {
     a = take_event(h);
     b = take_event(h);
-    if (a) cudaEventRecord(a, h->st);
+    if (a) cudaEventRecord(a, ts);
   }
   const cudaError_t e = f();
   if (timed && a && b) {
-    cudaEventRecord(b, h->st);
+    cudaEventRecord(b, ts);
     h->recs.push_back({id, a, b});
   }
   if (is_kernel && e == cudaSuccess) h->launches++;
@@ -339,8 +343,11 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.neg_cells = cfg->neg_obs_search_cells;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
-  if (cudaMemsetAsync(h->ws, 0, lay.total, h->st) != cudaSuccess) {
-    delete h;
+  if (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMemsetAsync(h->ws, 0, lay.total, h->st) != cudaSuccess) {
+    gvom_destroy(h);
     return GVOM_E_CUDA;
   }
   *out = h;
@@ -354,6 +361,9 @@ gvom_status gvom_destroy(gvom_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->aux) cudaStreamDestroy(h->aux);
   delete h;
   return GVOM_OK;
 }
@@ -429,6 +439,39 @@ static gvom_status stage_points(gvom_handle* h, const gvom_scan* scans, int32_t 
   return GVOM_OK;
 }
 
+// Ray cast a frame: sensors with the same ring count are batched (up to
+// kRayBatch) into one launch with interleaved azimuth tiles.
+static cudaError_t raycast_frame(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                 const std::vector<const float4*>& dptr, const SensorParams* sp,
+                                 uint32_t* miss, uint32_t* bits, const TileCounts& tc) {
+  std::vector<RayBatch> batches;
+  for (int i = 0; i < n_scans; ++i) {
+    if (scans[i].n == 0) continue;
+    const int32_t rings = scans[i].rings > 1 ? scans[i].rings : 0;
+    RayBatch* b = nullptr;
+    for (auto& x : batches)
+      if (x.rings == rings && x.S < kRayBatch) b = &x;
+    if (!b) {
+      batches.emplace_back();
+      b = &batches.back();
+      b->S = 0;
+      b->rings = rings;
+      b->tile_threads = rings > 1 ? 32 * (int64_t)rings : 32;
+    }
+    b->pts[b->S] = dptr[i];
+    b->n[b->S] = scans[i].n;
+    b->sp[b->S] = sp[i];
+    b->S++;
+  }
+  for (size_t k = 0; k < batches.size(); ++k) {
+    const cudaError_t e = stage(h, GVOM_STAGE_RAYCAST, true, [&] {
+      return launch_raycast(batches[k], h->d, miss, bits, tc, k + 1 == batches.size(), h->st);
+    });
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
   SensorParams sp[GVOM_MAX_SENSORS];
   const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
@@ -443,22 +486,12 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
   TileCounts tc = h->tc;
   tc.total = slot.meta;
-  int last_scan = -1;
-  for (int i = 0; i < n_scans; ++i)
-    if (scans[i].n > 0) last_scan = i;
   std::vector<const float4*> dptr;
   {
     const gvom_status st = stage_points(h, scans, n_scans, dptr);
     if (st != GVOM_OK) return st;
   }
-  for (int i = 0; i < n_scans; ++i) {
-    const gvom_scan& s = scans[i];
-    if (s.n == 0) continue;
-    GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
-      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, (uint32_t*)slot.lut, slot.bits, tc,
-                            i == last_scan, h->st);
-    }));
-  }
+  GVOM_CU(raycast_frame(h, scans, n_scans, dptr, sp, (uint32_t*)slot.lut, slot.bits, tc));
   // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
     return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st);
@@ -477,6 +510,23 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   return GVOM_OK;
 }
 
+// Layers from the surface: the cone search (+ Delta-H decision) on the aux
+// stream concurrently with the plane fits on the main stream (fork / join).
+static cudaError_t surface_layers(gvom_handle* h) {
+  cudaError_t e = cudaEventRecord(h->ev_fork, h->st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
+  if (e == cudaSuccess)
+    e = stage(h, GVOM_STAGE_NEGATIVE, true,
+              [&] { return launch_negative(h->d, h->lp, h->layers, h->aux); }, h->aux);
+  if (e == cudaSuccess) h->launches++;  // k_neg_decide
+  if (e == cudaSuccess)
+    e = stage(h, GVOM_STAGE_SLOPE, true,
+              [&] { return launch_slope(h->d, h->lp, h->layers, h->st); });
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_join, h->aux);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->st, h->ev_join, 0);
+  return e;
+}
+
 gvom_status gvom_compute_maps(gvom_handle* h) {
   if (!h) return GVOM_E_INVALID;
   if (h->count == 0) return GVOM_E_EMPTY;
@@ -488,10 +538,7 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
     return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st);
   }));
-  GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
-                [&] { return launch_negative(h->d, h->lp, h->layers, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
-                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
+  GVOM_CU(surface_layers(h));
   for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
   h->maps_valid = true;
   return GVOM_OK;
@@ -635,12 +682,10 @@ gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_
   GVOM_CU(cudaMemsetAsync(d_miss, 0, 4 * (size_t)d.V, h->st));
   GVOM_CU(cudaMemsetAsync(cnt, 0, 4 * (size_t)GVOM_MAX_RANKS, h->st));
   TileCounts none{};
+  GVOM_CU(raycast_frame(h, scans, n_scans, dptr, sp, d_miss, nullptr, none));
   for (int i = 0; i < n_scans; ++i) {
     const gvom_scan& s = scans[i];
     if (s.n == 0) continue;
-    GVOM_CU(stage(h, GVOM_STAGE_RAYCAST, true, [&] {
-      return launch_raycast(dptr[i], s.n, s.rings, sp[i], d, d_miss, nullptr, none, false, h->st);
-    }));
     GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true,
                   [&] { return launch_ep_count(dptr[i], s.n, sp[i], d, sb, cnt, h->st); }));
   }
@@ -747,10 +792,7 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
   }
   GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
                 [&] { return launch_transpose_init(h->d, h->layers, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
-                [&] { return launch_negative(h->d, h->lp, h->layers, h->st); }));
-  GVOM_CU(stage(h, GVOM_STAGE_SLOPE, true,
-                [&] { return launch_slope(h->d, h->lp, h->layers, h->st); }));
+  GVOM_CU(surface_layers(h));
   h->maps_valid = true;
   return GVOM_OK;
 }

@@ -79,9 +79,21 @@ __host__ __device__ inline int64_t n_tiles(const Dims& d) {
   return (d.V + (1 << kTileShift) - 1) >> kTileShift;
 }
 
-cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                           const Dims& d, uint32_t* miss_grid, uint32_t* bits,
-                           const TileCounts& tc, bool last_sensor, cudaStream_t st);
+// Up to kRayBatch sensors with the same ring count traced by one launch; their
+// 32-column tiles are interleaved (tile t of every sensor, then t+1, ...) so a
+// wave of warps covers one azimuth band of all sensors (voxels close together).
+constexpr int kRayBatch = 16;
+struct RayBatch {
+  int32_t S;      // sensors in the batch
+  int32_t rings;  // common ring count (<= 1: unstructured, one warp per tile)
+  int64_t tile_threads;
+  const float4* pts[kRayBatch];
+  int64_t n[kRayBatch];
+  SensorParams sp[kRayBatch];
+};
+cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_grid,
+                           uint32_t* bits, const TileCounts& tc, bool last_launch,
+                           cudaStream_t st);
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,

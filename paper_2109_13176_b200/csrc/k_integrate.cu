@@ -187,12 +187,18 @@ __device__ __forceinline__ void aggregate_red(uint32_t* __restrict__ miss, uint3
 }
 
 template <bool kMatchAgg, bool kAggFirst>
-__global__ void __launch_bounds__(256) k_raycast(const float4* __restrict__ pts, int64_t n,
-                                                 int32_t rings, const SensorParams sp,
+__global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatch rb,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gt = gtid / rb.tile_threads;  // interleaved (tile, sensor)
+  const int sidx = (int)(gt % rb.S);
+  const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
+  const int rings = rb.rings;
+  const int64_t n = rb.n[sidx];
+  const float4* __restrict__ pts = rb.pts[sidx];
+  const SensorParams sp = rb.sp[sidx];
   const int64_t p = point_index(tid, rings);
   const int lane = threadIdx.x & 31;
   const float s0 = sp.b[0], s1 = sp.b[1], s2 = sp.b[2];
@@ -766,36 +772,22 @@ inline int64_t point_threads(int64_t n, int32_t rings) {
 
 }  // namespace
 
-cudaError_t launch_raycast(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                           const Dims& d, uint32_t* miss_grid, uint32_t* bits,
-                           const TileCounts& tc, bool last_sensor, cudaStream_t st) {
-  const int64_t threads = point_threads(n, rings);
+cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_grid,
+                           uint32_t* bits, const TileCounts& tc, bool last_launch,
+                           cudaStream_t st) {
+  int64_t tiles = 0;  // per sensor, the batch's maximum
+  for (int s = 0; s < rb.S; ++s) {
+    const int64_t t = (point_threads(rb.n[s], rb.rings) + rb.tile_threads - 1) / rb.tile_threads;
+    tiles = t > tiles ? t : tiles;
+  }
+  const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
-  // small blocks: a frame is one wave of warps; many small blocks spread the
-  // long (upward / horizontal) and short (ground) rings evenly over the SMs
-  static const int bs = [] {
-    const char* e = getenv("GVOM_RAY_BLOCK");
-    const int v = e ? atoi(e) : 64;
-    return (v >= 32 && v <= 256 && v % 32 == 0) ? v : 64;
-  }();
-  static const bool match = [] {
-    const char* e = getenv("GVOM_RAY_AGG");
-    return e && e[0] == 'm';
-  }();
+  // small blocks: a frame is about one wave of warps; many small blocks spread
+  // the long (upward / horizontal) and short (ground) rings over the SMs
+  constexpr int bs = 64;
   const int64_t blocks = (threads + bs - 1) / bs;
-  static const bool ddafirst = [] {
-    const char* e = getenv("GVOM_RAY_ORDER");
-    return e && e[0] == 'd';
-  }();
-  if (match)
-    k_raycast<true, true><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits,
-                                                           tc, last_sensor);
-  else if (ddafirst)
-    k_raycast<false, false><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid,
-                                                             bits, tc, last_sensor);
-  else
-    k_raycast<false, true><<<(unsigned)blocks, bs, 0, st>>>(pts, n, rings, sp, d, miss_grid, bits,
-                                                            tc, last_sensor);
+  k_raycast<false, true><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc,
+                                                          last_launch);
   return cudaGetLastError();
 }
 

@@ -239,15 +239,10 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   const int cx = threadIdx.x + kSlopeHalo, cy = threadIdx.y + kSlopeHalo;
   const int32_t qc = tile[cy][cx];
   if (qc == kQsUndef) {
-    // O10 decision for an undefined cell from the cone sweeps' min / max:
-    // max F - min F > T_neg (>= 0, so it implies |F| >= 2)
-    const int32_t mn = __ldg(out.nmin + c), mx = __ldg(out.nmax + c);
-    out.neg[c] = (mx != INT32_MIN && (int64_t)mx - (int64_t)mn > lp.T_neg) ? 1 : 0;
     out.slope[c] = qnan;
     out.rough[c] = qnan;
     return;
   }
-  out.neg[c] = 0;
   int32_t n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0;
   int64_t Sz = 0, Suz = 0, Svz = 0;
   for (int v = -r; v <= r; ++v)
@@ -311,8 +306,7 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
 // nmin / nmax with atomics, and k_slope applies "max - min > T_neg".
 // Lines are streamed into a shared-memory ring by 1D TMA bulk copies
 // (cp.async.bulk, mbarrier completion) kNegRing lines ahead of the sweep.
-constexpr int kNegThreads = 512;
-constexpr int kNegRing = 8;
+constexpr int kNegRing = 32;
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
@@ -351,10 +345,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(kNegThreads) k_negative(const Dims d, const LayerParams lp,
-                                                          const LayerPtrs out, int T) {
+// Warp-specialised: the last warp is the producer (TMA bulk copies of the
+// ring-1 lines, kNegRing slots ahead, guarded by full/empty mbarriers); the
+// other warps are consumers (one apex position each per pass) and sync among
+// themselves with a named barrier once per line.
+__global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerParams lp,
+                                                        const LayerPtrs out, int T) {
   extern __shared__ __align__(16) int32_t sm[];
-  __shared__ __align__(8) uint64_t bars[kNegRing];
+  __shared__ __align__(8) uint64_t full[kNegRing], empty[kNegRing];
   const int cone = blockIdx.y;               // 0:+x 1:-x 2:+y 3:-y
   const bool alongx = cone < 2;              // sweep over x (lines = columns)
   const int dir = (cone & 1) ? -1 : 1;       // ring lines lie at p + dir*k
@@ -363,6 +361,7 @@ __global__ void __launch_bounds__(kNegThreads) k_negative(const Dims d, const La
   const int K = lp.neg_cells;
   const int NB = B + 2 * K + 2;              // apex cross positions -K-1 .. B+K
   const int BP = (B + 3) & ~3;               // ring line stride (16-byte rows)
+  const int nthr = blockDim.x - 32;          // consumer threads
   int32_t* ring = sm;                        // [kNegRing][BP]
   int32_t* Dp = ring + kNegRing * BP;        // state of the previous line
   int32_t* Dn = Dp + NB;
@@ -385,42 +384,48 @@ __global__ void __launch_bounds__(kNegThreads) k_negative(const Dims d, const La
   }
   const bool tma = (B & 3) == 0;             // rows are whole 16-byte chunks
   const uint32_t line_bytes = (uint32_t)B * 4u;
-  // step s reads ring-1 line pl(s) = pstart - dir*s + dir
-  auto line_of = [&](int st) { return pstart - dir * st + dir; };
+  auto line_of = [&](int st) { return pstart - dir * st + dir; };  // ring-1 line of step st
   for (int i = threadIdx.x; i < NB; i += blockDim.x) {
     Dp[i] = Dn[i] = INF;  // both buffers: guard cells are never rewritten
     Mnp[i] = Mnn[i] = INT32_MAX;
     Mxp[i] = Mxn[i] = INT32_MIN;
   }
   if (threadIdx.x == 0) {
-    for (int j = 0; j < kNegRing; ++j) mbar_init(&bars[j], 1);
+    for (int j = 0; j < kNegRing; ++j) {
+      mbar_init(&full[j], 1);
+      mbar_init(&empty[j], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tma && threadIdx.x == 0) {
-    for (int j = 0; j < kNegRing && j < nsteps; ++j) {
-      const int pl = line_of(j);
-      if (pl >= 0 && pl < A)
-        tma_line(ring + j * BP, src + (int64_t)pl * B, line_bytes, &bars[j]);
-      else
-        mbar_arrive(&bars[j]);
+  if (threadIdx.x >= nthr) {
+    // ---------------- producer warp ----------------
+    if (threadIdx.x == nthr) {
+      for (int st = 0; st < nsteps; ++st) {
+        const int j = st % kNegRing;
+        if (st >= kNegRing) mbar_wait(&empty[j], (uint32_t)(((st / kNegRing) - 1) & 1));
+        const int pl = line_of(st);
+        if (tma && pl >= 0 && pl < A)
+          tma_line(ring + j * BP, src + (int64_t)pl * B, line_bytes, &full[j]);
+        else
+          mbar_arrive(&full[j]);
+      }
     }
+    return;
   }
+  // ---------------- consumers ----------------
   for (int st = 0; st < nsteps; ++st) {
     const int p = pstart - dir * st;
     const int pl = p + dir;
     const bool inmap = pl >= 0 && pl < A;
     const int j = st % kNegRing;
     int32_t* lq = ring + j * BP;
-    if (inmap) {
-      if (tma) {
-        mbar_wait(&bars[j], (uint32_t)((st / kNegRing) & 1));
-      } else {
-        for (int b = threadIdx.x; b < B; b += blockDim.x) lq[b] = __ldg(src + (int64_t)pl * B + b);
-        __syncthreads();
-      }
+    mbar_wait(&full[j], (uint32_t)((st / kNegRing) & 1));
+    if (inmap && !tma) {  // rows not 16-byte multiples: plain loads
+      for (int b = threadIdx.x; b < B; b += nthr) lq[b] = __ldg(src + (int64_t)pl * B + b);
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr));
     }
-    for (int i = threadIdx.x + 1; i < NB - 1; i += blockDim.x) {
+    for (int i = threadIdx.x + 1; i < NB - 1; i += nthr) {
       const int b = i - K - 1;  // apex cross position
       int Dv = INF, mn = INT32_MAX, mx = INT32_MIN;
       if (inmap) {  // ring 1: cross b-1..b+1 of line pl (in-map only)
@@ -456,18 +461,25 @@ __global__ void __launch_bounds__(kNegThreads) k_negative(const Dims d, const La
         atomicMax(out.nmax + cell, mx);
       }
     }
-    __syncthreads();  // state + ring slot j fully consumed
-    if (tma && threadIdx.x == 0 && st + kNegRing < nsteps) {
-      const int pn = line_of(st + kNegRing);
-      if (pn >= 0 && pn < A)
-        tma_line(lq, src + (int64_t)pn * B, line_bytes, &bars[j]);
-      else
-        mbar_arrive(&bars[j]);
-    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");  // state + slot j consumed
+    if (threadIdx.x == 0) mbar_arrive(&empty[j]);
     int32_t* t0 = Dp; Dp = Dn; Dn = t0;
     t0 = Mnp; Mnp = Mnn; Mnn = t0;
     t0 = Mxp; Mxp = Mxn; Mxn = t0;
   }
+}
+
+// O10 decision from the cone sweeps' min / max: undefined cell and
+// max F - min F > T_neg (T_neg >= 0, so this implies |F| >= 2, reading B2)
+__global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerParams lp,
+                                                    const LayerPtrs out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)d.nx * d.ny) return;
+  const int32_t mn = __ldg(out.nmin + c), mx = __ldg(out.nmax + c);
+  out.neg[c] = (__ldg(out.qs + c) == kQsUndef && mx != INT32_MIN &&
+                (int64_t)mx - (int64_t)mn > lp.T_neg)
+                   ? 1
+                   : 0;
 }
 
 // merged occupancy bits of the combined map (export path)
@@ -598,8 +610,14 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
         k_negative, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  // consumers: one apex position each per pass (up to 1024), + 1 producer warp
+  int nthr = (int)((NB - 2 + 31) / 32) * 32;
+  if (nthr > 1024 - 32) nthr = 1024 - 32;  // + the producer warp <= 1024 threads
   const dim3 grid((unsigned)((A + T - 1) / T), 4);
-  k_negative<<<grid, kNegThreads, smem, st>>>(d, lp, out, T);
+  k_negative<<<grid, nthr + 32, smem, st>>>(d, lp, out, T);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_neg_decide<<<cells_blocks(d, 256), 256, 0, st>>>(d, lp, out);
   return cudaGetLastError();
 }
 
