@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--frames", type=int, default=4, help="distinct scans cycled")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
+    ap.add_argument("--slab", action="store_true",
+                    help="multi-GPU slab partition of one frame (default for --config 4, N > 1)")
     return ap.parse_args()
 
 
@@ -206,6 +208,76 @@ def run_reference(args):
     return 0
 
 
+def main_slab(args):
+    """the points of ONE frame are sharded across the ranks (sensor
+    i -> rank i % N); miss grids are reduce-scattered by y-slab over NCCL,
+    returns routed to slab owners, surface rows all-gathered.  Strong scaling:
+    value = points of the whole frame per second (max-over-ranks time)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_13176_b200 import GvomMap, parallel
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    w = load_workload(args.config, args.frames, 0)  # the same frame on every rank
+    f = w.frames[0]
+    grid = dict(w.grid)
+    grid["buffer_frames"] = 1
+    mine = [(torch.from_numpy(s.points).to(dev), s.pose, s.rings)
+            for i, s in enumerate(f.scans) if i % world == rank]
+    npts_all = f.n_points
+    stream = torch.cuda.Stream(device=dev)
+    m = GvomMap(grid, max_points_per_frame=max(1, sum(x[0].shape[0] for x in mine)), device=dev,
+                stream=stream)
+    sm = parallel.SlabMapper(m, ep_capacity=npts_all)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        m.shift(f.vehicle_xyz)
+        sm.integrate(mine)
+        sm.compute_maps()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        total = 0.0
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                step()
+                b.record(stream)
+                b.synchronize()
+                total += a.elapsed_time(b)
+        dist.barrier()
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t[0])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": npts_all * args.steps / (total / 1e3), "unit": "points/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
+            "config": {"workload": w.name, "points_per_frame": npts_all, "sensors": len(f.scans),
+                       "grid": f"{m.nx}x{m.ny}x{m.nz}@{w.grid['res']}m", "buffer_frames": 1,
+                       "parallelism": f"slab{world}: sensors sharded, reduce-scatter by y-slab",
+                       "l2": "flushed (256 MiB write) between steps",
+                       "step": "shift+partial_scan+exchange+slab_finalize+slab maps"},
+            "map_updates_per_s": args.steps / (total / 1e3),
+            "gpu_launches": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -214,6 +286,8 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if args.slab or (args.config == 4 and world > 1):
+        return main_slab(args)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
     torch.cuda.set_device(local)
