@@ -56,12 +56,20 @@ typedef enum gvom_status {
 /* Map and layer parameters.  The paper names these but gives values only for
  * the map size and resolution ("typically [256,256,64] with a
  * resolution of 40 cm"); defaults are in DESIGN.md "Parameters". */
+/* Pipelined mode ("Both of these processes can be run asynchronously"):
+ * map processing (compute_maps, export_2d / export_layers) runs on the
+ * handle's own map stream (gvom_map_stream) so integrate_scan of the next scan
+ * overlaps compute_maps of this one.  One spare buffer slot is allocated; the
+ * slot an integrate overwrites is fenced on the compute_maps that last read
+ * it.  Results of compute_maps / exports are ordered on the map stream.      */
+#define GVOM_FLAG_PIPELINE 1
+
 typedef struct gvom_config {
   int32_t nx, ny, nz;            /* voxels, each >= 1, nz <= 2048, nx*ny*nz < 2^31 */
   double res;                    /* metres per voxel edge, > 0                    */
   double z_center_frac;          /* vehicle z at floor(nz*frac) voxels (reading A3)      */
   int32_t buffer_frames;         /* K per-scan maps kept ("the buffer"), 1..32       */
-  int32_t pad0;
+  int32_t flags;                 /* GVOM_FLAG_* (0: default)                              */
   int64_t max_points_per_frame;  /* capacity: points of all sensors of one frame          */
   double min_obstacle_height;    /* metres above the surface                     */
   double max_obstacle_height;    /* metres above the surface                     */
@@ -213,6 +221,9 @@ GVOM_API gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
                                         int64_t n_ep);
 GVOM_API gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1,
                                             int32_t phase);
+/* the stream map processing is enqueued on (the handle's stream unless
+ * GVOM_FLAG_PIPELINE): consumers of layers order themselves after it      */
+GVOM_API gvom_status gvom_map_stream(gvom_handle* h, void** out_stream);
 /* device pointer of the [ny][nx] int32 surface buffer (q_s, INT32_MIN = none) */
 GVOM_API gvom_status gvom_surface_buffer(gvom_handle* h, int32_t** out_d_qs);
 

@@ -50,6 +50,7 @@ bool valid_config(const gvom_config* c) {
   if (c->slope_window < 3 || c->slope_window > 9 || (c->slope_window % 2) == 0) return false;
   if (c->min_plane_points < 3) return false;
   if (!(c->neg_obs_threshold >= 0) || c->neg_obs_search_cells < 1) return false;
+  if (c->flags & ~GVOM_FLAG_PIPELINE) return false;
   return true;
 }
 
@@ -76,7 +77,9 @@ Layout make_layout(const gvom_config* c) {
   l.slot_data = l.slot_wprefix + align_up(4 * (size_t)d.W);
   l.slot_meta = l.slot_data + align_up(sizeof(gvom_voxel) * (size_t)(l.cap > 0 ? l.cap : 1));
   l.slot_stride = l.slot_meta + kAlign;
-  off = l.slot_stride * (size_t)c->buffer_frames;
+  // one spare slot when pipelined: integrate(t+1) writes it while
+  // compute_maps(t) still reads the K newest
+  off = l.slot_stride * (size_t)(c->buffer_frames + ((c->flags & GVOM_FLAG_PIPELINE) ? 1 : 0));
   l.staging = off;
   off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
   l.rank_tmp = off;
@@ -142,6 +145,16 @@ struct gvom_handle {
   // fork/join: the cone search runs on `aux` while k_slope runs on `st`
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // pipelined mode (GVOM_FLAG_PIPELINE): map processing on its own stream
+  bool pipelined = false;
+  int NS = 0;                       // physical slots: K (+1 when pipelined)
+  cudaStream_t mst = nullptr;       // map stream (pipelined)
+  cudaEvent_t ev_integrated = nullptr;
+  static constexpr int kMapsRing = 4;
+  cudaEvent_t ev_maps[kMapsRing] = {};
+  int64_t maps_calls = 0;           // compute_maps calls so far
+  std::vector<int64_t> slot_reader; // last compute_maps call that read a slot
+  cudaStream_t ms() const { return pipelined ? mst : st; }
 };
 
 namespace {
@@ -242,9 +255,10 @@ SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
   ss.kp_log2 = 0;
   while ((1 << ss.kp_log2) < ss.K) ss.kp_log2++;
   for (int age = 0; age < h->count; ++age) {
-    const int idx = ((h->head - 1 - age) % h->K + h->K) % h->K;
+    const int idx = ((h->head - 1 - age) % h->NS + h->NS) % h->NS;
     const Slot& s = h->slots[idx];
     SlotView& v = ss.s[age];
+    h->slot_reader[idx] = h->maps_calls;  // this compute_maps reads the slot
     v.lut = s.lut;
     v.bits = s.bits;
     v.wprefix = s.wprefix;
@@ -303,8 +317,11 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->st = (cudaStream_t)cuda_stream;
   h->ws = (char*)d_workspace;
   h->K = cfg->buffer_frames;
-  h->slots.resize(h->K);
-  for (int k = 0; k < h->K; ++k) {
+  h->pipelined = (cfg->flags & GVOM_FLAG_PIPELINE) != 0;
+  h->NS = h->K + (h->pipelined ? 1 : 0);
+  h->slots.resize(h->NS);
+  h->slot_reader.assign(h->NS, -1);
+  for (int k = 0; k < h->NS; ++k) {
     char* b = h->ws + lay.slot_stride * (size_t)k;
     Slot& s = h->slots[k];
     s.lut = (int32_t*)(b + lay.slot_lut);
@@ -343,7 +360,14 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.neg_cells = cfg->neg_obs_search_cells;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
-  if (cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
+  bool ok = true;
+  if (h->pipelined) {
+    ok = cudaStreamCreateWithFlags(&h->mst, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&h->ev_integrated, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < gvom_handle::kMapsRing; ++i)
+      ok = cudaEventCreateWithFlags(&h->ev_maps[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+  if (!ok || cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(h->ws, 0, lay.total, h->st) != cudaSuccess) {
@@ -364,6 +388,10 @@ gvom_status gvom_destroy(gvom_handle* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_integrated) cudaEventDestroy(h->ev_integrated);
+  for (auto e : h->ev_maps)
+    if (e) cudaEventDestroy(e);
+  if (h->mst) cudaStreamDestroy(h->mst);
   delete h;
   return GVOM_OK;
 }
@@ -377,6 +405,7 @@ gvom_status gvom_set_stream(gvom_handle* h, void* cuda_stream) {
 gvom_status gvom_synchronize(gvom_handle* h) {
   if (!h) return GVOM_E_INVALID;
   GVOM_CU(cudaStreamSynchronize(h->st));
+  if (h->mst) GVOM_CU(cudaStreamSynchronize(h->mst));
   return GVOM_OK;
 }
 
@@ -439,6 +468,15 @@ static gvom_status stage_points(gvom_handle* h, const gvom_scan* scans, int32_t 
   return GVOM_OK;
 }
 
+// Pipelined mode: before integrate overwrites slot j, the main stream waits
+// for the last compute_maps that read it (or a later one: same map stream).
+static cudaError_t wait_slot_readers(gvom_handle* h, int j) {
+  if (!h->pipelined || h->slot_reader[j] < 0) return cudaSuccess;
+  int64_t r = h->slot_reader[j];
+  if (h->maps_calls - r > gvom_handle::kMapsRing) r = h->maps_calls - gvom_handle::kMapsRing;
+  return cudaStreamWaitEvent(h->st, h->ev_maps[r % gvom_handle::kMapsRing], 0);
+}
+
 // Ray cast a frame: sensors with the same ring count are batched (up to
 // kRayBatch) into one launch with interleaved azimuth tiles.
 static cudaError_t raycast_frame(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
@@ -478,6 +516,7 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   if (ps != GVOM_OK) return ps;
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
+  GVOM_CU(wait_slot_readers(h, h->head));
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
     return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
                         (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
@@ -505,40 +544,46 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     }));
   }
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
-  h->head = (h->head + 1) % h->K;
+  h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
+  if (h->pipelined) GVOM_CU(cudaEventRecord(h->ev_integrated, h->st));
   return GVOM_OK;
 }
 
 // Layers from the surface: the cone search (+ Delta-H decision) on the aux
 // stream concurrently with the plane fits on the main stream (fork / join).
 static cudaError_t surface_layers(gvom_handle* h) {
-  cudaError_t e = cudaEventRecord(h->ev_fork, h->st);
+  cudaError_t e = cudaEventRecord(h->ev_fork, h->ms());
   if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
   if (e == cudaSuccess)
     e = stage(h, GVOM_STAGE_NEGATIVE, true,
               [&] { return launch_negative(h->d, h->lp, h->layers, h->aux); }, h->aux);
   if (e == cudaSuccess) h->launches++;  // k_neg_decide
   if (e == cudaSuccess)
-    e = stage(h, GVOM_STAGE_SLOPE, true,
-              [&] { return launch_slope(h->d, h->lp, h->layers, h->st); });
+    e = stage(
+        h, GVOM_STAGE_SLOPE, true, [&] { return launch_slope(h->d, h->lp, h->layers, h->ms()); },
+        h->ms());
   if (e == cudaSuccess) e = cudaEventRecord(h->ev_join, h->aux);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->st, h->ev_join, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->ms(), h->ev_join, 0);
   return e;
 }
 
 gvom_status gvom_compute_maps(gvom_handle* h) {
   if (!h) return GVOM_E_INVALID;
   if (h->count == 0) return GVOM_E_EMPTY;
-  const int newest = (h->head - 1 + h->K) % h->K;
+  const int newest = (h->head - 1 + h->NS) % h->NS;
   int64_t o[3];
   for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
+  if (h->pipelined) GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated, 0));
   h->map_slots = buffer_slots(h, o);
   h->lp.o_z = o[2];
-  GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
-    return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st);
-  }));
+  GVOM_CU(stage(
+      h, GVOM_STAGE_COLUMNS, true,
+      [&] { return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->ms()); }, h->ms()));
   GVOM_CU(surface_layers(h));
+  if (h->pipelined)
+    GVOM_CU(cudaEventRecord(h->ev_maps[h->maps_calls % gvom_handle::kMapsRing], h->mst));
+  h->maps_calls++;
   for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
   h->maps_valid = true;
   return GVOM_OK;
@@ -574,14 +619,15 @@ gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT]
     if (((uintptr_t)dst[l] & 15) != 0 || !is_device_ptr(dst[l])) one_kernel = false;
   }
   if (one_kernel) {
-    GVOM_CU(stage(h, GVOM_STAGE_EXPORT, true, [&] { return launch_export_layers(job, h->st); }));
+    GVOM_CU(stage(
+        h, GVOM_STAGE_EXPORT, true, [&] { return launch_export_layers(job, h->ms()); }, h->ms()));
     return GVOM_OK;
   }
   for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
     GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
       return cudaMemcpyAsync(job.dst[l], job.src[l], (size_t)job.bytes[l], cudaMemcpyDefault,
-                             h->st);
-    }));
+                             h->ms());
+    }, h->ms()));
   }
   return GVOM_OK;
 }
@@ -595,7 +641,7 @@ gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t d
   const size_t bytes = elem * (size_t)h->lay.cells;
   if (dst_bytes < bytes) return GVOM_E_SIZE;
   GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
-    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->st);
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->ms());
   }));
   return GVOM_OK;
 }
@@ -612,6 +658,7 @@ gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_dat
   if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
   const Dims& d = h->d;
+  if (h->mst) GVOM_CU(cudaStreamSynchronize(h->mst));
   GVOM_CU(cudaMemsetAsync(h->mbits, 0, 4 * (size_t)d.W, h->st));
   GVOM_CU(stage(h, GVOM_STAGE_MERGE, true,
                 [&] { return launch_merge_bits(h->map_slots, d, h->mbits, h->st); }));
@@ -634,8 +681,9 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
                               int64_t cap, int64_t* out_k, int64_t out_origin[3]) {
   if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
   if (age < 0 || age >= h->count) return GVOM_E_EMPTY;
-  const int idx = ((h->head - 1 - age) % h->K + h->K) % h->K;
+  const int idx = ((h->head - 1 - age) % h->NS + h->NS) % h->NS;
   const Slot& s = h->slots[idx];
+  if (h->mst) GVOM_CU(cudaStreamSynchronize(h->mst));
   uint32_t k = 0;
   GVOM_CU(cudaMemcpyAsync(&k, s.meta, 4, cudaMemcpyDeviceToHost, h->st));
   GVOM_CU(cudaStreamSynchronize(h->st));
@@ -653,7 +701,7 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
 
 // ---- multi-GPU slab partition --------------------------------
 static bool slab_ok(const gvom_handle* h, int32_t y0, int32_t y1) {
-  return h && h->cfg.buffer_frames == 1 && y0 >= 0 && y1 <= h->cfg.ny && y0 < y1;
+  return h && h->cfg.buffer_frames == 1 && !h->pipelined && y0 >= 0 && y1 <= h->cfg.ny && y0 < y1;
 }
 
 gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
@@ -768,7 +816,7 @@ gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uin
     return launch_endpoint_records((const EpRecord*)d_ep, n_ep, slot.lut, slot.data, h->st);
   }));
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
-  h->head = (h->head + 1) % h->K;
+  h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
   h->slab_y0 = h->slab_y1 = -1;
   return GVOM_OK;
@@ -778,7 +826,7 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
   if (!slab_ok(h, y0, y1) || (phase != 0 && phase != 1)) return GVOM_E_INVALID;
   if (h->count == 0) return GVOM_E_EMPTY;
   if (phase == 0) {
-    const int newest = (h->head - 1 + h->K) % h->K;
+    const int newest = (h->head - 1 + h->NS) % h->NS;
     int64_t o[3];
     for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
     h->map_slots = buffer_slots(h, o);
@@ -794,6 +842,12 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
                 [&] { return launch_transpose_init(h->d, h->layers, h->st); }));
   GVOM_CU(surface_layers(h));
   h->maps_valid = true;
+  return GVOM_OK;
+}
+
+gvom_status gvom_map_stream(gvom_handle* h, void** out_stream) {
+  if (!h || !out_stream) return GVOM_E_INVALID;
+  *out_stream = (void*)h->ms();
   return GVOM_OK;
 }
 

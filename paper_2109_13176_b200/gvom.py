@@ -43,7 +43,7 @@ class SensorOutside(GvomError):
 
 class Config(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("res", C.c_double),
-                ("z_center_frac", C.c_double), ("buffer_frames", C.c_int32), ("pad0", C.c_int32),
+                ("z_center_frac", C.c_double), ("buffer_frames", C.c_int32), ("flags", C.c_int32),
                 ("max_points_per_frame", C.c_int64), ("min_obstacle_height", C.c_double),
                 ("max_obstacle_height", C.c_double), ("density_threshold", C.c_double),
                 ("slope_window", C.c_int32), ("min_plane_points", C.c_int32),
@@ -101,6 +101,7 @@ def load_library() -> C.CDLL:
         "gvom_slab_finalize": ([P, I32, I32, P, P, I64], I32),
         "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
         "gvom_surface_buffer": ([P, P], I32),
+        "gvom_map_stream": ([P, P], I32),
         "gvom_abi_version": ([], I32),
     }
     for name, (args, res) in sig.items():
@@ -116,7 +117,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_export_2d", "gvom_export_layers", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
-            "gvom_compute_maps_slab", "gvom_surface_buffer")
+            "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -125,6 +126,7 @@ def make_config(grid: dict, max_points_per_frame: int) -> Config:
     c.res = float(grid["res"])
     c.z_center_frac = float(grid.get("z_center_frac", 0.5))
     c.buffer_frames = int(grid.get("buffer_frames", 8))
+    c.flags = 1 if grid.get("pipeline", False) else 0  # GVOM_FLAG_PIPELINE
     c.max_points_per_frame = int(max_points_per_frame)
     c.min_obstacle_height = float(grid["min_obstacle_height"])
     c.max_obstacle_height = float(grid["max_obstacle_height"])
@@ -253,6 +255,15 @@ class GvomMap:
 
     def compute_maps_slab(self, y0: int, y1: int, phase: int):
         _check(self.lib.gvom_compute_maps_slab(self.h, y0, y1, phase), "gvom_compute_maps_slab")
+
+    @property
+    def map_stream(self) -> torch.cuda.Stream:
+        """Stream that map processing and exports are ordered on."""
+        ptr = C.c_void_p()
+        _check(self.lib.gvom_map_stream(self.h, C.byref(ptr)), "gvom_map_stream")
+        if ptr.value == self.stream.cuda_stream:
+            return self.stream
+        return torch.cuda.ExternalStream(ptr.value, device=self.device)
 
     def surface(self) -> torch.Tensor:
         """int32 [ny, nx] view of the library's surface buffer (q_s; INT32_MIN = none)."""

@@ -67,9 +67,9 @@ def compare_merged(m: GvomMap, om: "O.OracleMap"):
 
 
 def layers_np(m: GvomMap) -> dict:
-    out = {k: v.cpu().numpy() for k, v in m.export_layers().items()}
-    m.synchronize()
-    return out
+    lay = m.export_layers()
+    m.synchronize()  # exports are ordered on the map stream (pipelined mode)
+    return {k: v.cpu().numpy() for k, v in lay.items()}
 
 
 def run_sequence(w, frames=None, *, host=False, check_every=1, check_merged=True,

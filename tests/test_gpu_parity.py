@@ -166,3 +166,32 @@ def test_c5_large_map_full_size():
     # 8 streams x 524,288 points, 1024x1024x128 voxels at 0.1 m, K = 1.
     # The oracle runs the whole frame (~30 s single-threaded C).
     run_sequence(synth.workload(4), check_merged=False)
+
+
+@pytest.mark.parametrize("speed", [12.0])
+def test_pipelined_mode_overlapping_frames(speed):
+    # GVOM_FLAG_PIPELINE (P:88 asynchronous pointcloud / map processing): every
+    # frame is enqueued without waiting -- integrate(t+1) on the handle stream
+    # overlaps compute_maps(t) + export(t) on the map stream -- and each frame's
+    # layers land in their own buffers; all are compared with the oracle after
+    # a single synchronize.  Exercises the spare slot and the slot fences.
+    w = synth.config3(speed=speed, n_frames=11, columns=1024)
+    g = dict(w.grid)
+    g["pipeline"] = True
+    m = GvomMap(g, max_points_per_frame=w.points_per_frame)
+    assert m.map_stream.cuda_stream != m.stream.cuda_stream
+    om = O.OracleMap(w.grid)
+    dev = [[to_dev(s) for s in f.scans] for f in w.frames]
+    outs, refs = [], []
+    for i, f in enumerate(w.frames):
+        m.shift(f.vehicle_xyz)
+        m.integrate_scan(dev[i])
+        m.compute_maps()
+        outs.append(m.export_layers())
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in f.scans])
+        refs.append(om.compute_maps())
+    m.synchronize()
+    for got, ref in zip(outs, refs):
+        compare_layers({k: v.cpu().numpy() for k, v in got.items()}, ref)
+    compare_merged(m, om)
