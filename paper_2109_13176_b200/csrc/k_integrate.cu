@@ -179,11 +179,12 @@ __device__ __forceinline__ void aggregate_red(uint32_t* __restrict__ miss, uint3
     const unsigned heads = __ballot_sync(0xffffffffu, head);
     cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
   }
+  // no "memory" clobber: nothing in the kernel reads the miss grid, so the
+  // reduction needs no ordering with the surrounding code
   asm volatile(
       "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
       "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
-      "r"(cnt), "r"((uint32_t)head)
-      : "memory");
+      "r"(cnt), "r"((uint32_t)head));
 }
 
 template <bool kMatchAgg, bool kAggFirst>
@@ -652,43 +653,56 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
   if (w < d.W) wprefix[w] = pre;
   if (blockIdx.x == gridDim.x - 1 && t == kTileWords - 1) *tc.total = pre + c;  // k of the frame
   __syncthreads();
-  // voxels of the tile, 4 per thread per iteration
+  // voxels of the tile: 8 x 16-byte chunks per thread, all loads in flight
+  // before any store (the tile is whole unless it is the grid's last)
   const int64_t vbase = b << kTileShift;
+  constexpr int kIt = (1 << kTileShift) / (kTileWords * 4);  // 8
+  if (vbase + (1 << kTileShift) <= d.V) {
+    uint4 mv[kIt];
+#pragma unroll
+    for (int it = 0; it < kIt; ++it)
+      mv[it] = __ldcs(reinterpret_cast<const uint4*>(buf + vbase + t * 4 + it * kTileWords * 4));
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int i = t * 4 + it * kTileWords * 4;
+      const uint32_t ww = sbits[i >> 5], pp = spre[i >> 5];
+      const uint32_t m[4] = {mv[it].x, mv[it].y, mv[it].z, mv[it].w};
+      int32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int bit = (i + j) & 31;
+        if ((ww >> bit) & 1u) {
+          const uint32_t rank = pp + __popc(ww & ((1u << bit) - 1u));
+          o[j] = (int32_t)rank;
+          uint4* row = reinterpret_cast<uint4*>(data + rank);
+          row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
+          row[1] = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          o[j] = -1 - (int32_t)(m[j] < kMissSat ? m[j] : kMissSat);
+        }
+      }
+      *reinterpret_cast<int4*>(buf + vbase + i) = make_int4(o[0], o[1], o[2], o[3]);
+    }
+    return;
+  }
   for (int i = t * 4; i < (1 << kTileShift); i += kTileWords * 4) {
     const int64_t L = vbase + i;
     if (L >= d.V) break;
     const uint32_t ww = sbits[i >> 5], pp = spre[i >> 5];
-    const bool vec = (L + 3 < d.V);
     uint32_t m[4];
-    if (vec) {
-      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(buf + L));
-      m[0] = v.x;
-      m[1] = v.y;
-      m[2] = v.z;
-      m[3] = v.w;
-    } else {
-      for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
-    }
-    int32_t o[4];
-#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
     for (int j = 0; j < 4; ++j) {
+      if (L + j >= d.V) break;
       const int bit = (i + j) & 31;
       if ((ww >> bit) & 1u) {
         const uint32_t rank = pp + __popc(ww & ((1u << bit) - 1u));
-        o[j] = (int32_t)rank;
+        buf[L + j] = (int32_t)rank;
         uint4* row = reinterpret_cast<uint4*>(data + rank);
         row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
         row[1] = make_uint4(0u, 0u, 0u, 0u);
       } else {
-        const uint32_t nm = m[j] < kMissSat ? m[j] : kMissSat;
-        o[j] = -1 - (int32_t)nm;
+        buf[L + j] = -1 - (int32_t)(m[j] < kMissSat ? m[j] : kMissSat);
       }
-    }
-    if (vec) {
-      *reinterpret_cast<int4*>(buf + L) = make_int4(o[0], o[1], o[2], o[3]);
-    } else {
-      for (int j = 0; j < 4; ++j)
-        if (L + j < d.V) buf[L + j] = o[j];
     }
   }
 }
