@@ -173,6 +173,15 @@ GVOM_API gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst,
 GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
                                         const size_t dst_bytes[GVOM_LAYER_COUNT]);
 
+/* Costmap ("each of the output maps get some weight assigned to them
+ * and the resulting per pixel sum is the cost in that pixel"; SURVEY 8(f)
+ * NEXT-4).  cost = w0*hard + w1*soft + w2*density + w3*negative + w4*slope
+ * + w5*roughness + w6*unknown, f32 in that order; a NaN layer contributes 0;
+ * unknown = height undefined and not a negative obstacle (reading B5).
+ * dst: nx*ny float32, host or device; ordered on the map stream.          */
+GVOM_API gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst,
+                                  size_t dst_bytes);
+
 /* World-voxel origin of the last compute_maps (newest buffer map).  */
 GVOM_API gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]);
 

@@ -471,3 +471,27 @@ void or_negative(int32_t nx, int32_t ny, int32_t K, int64_t T_neg, const int32_t
       neg[c] = (fcount >= 2 && (fmax - fmin) > T_neg) ? 1 : 0;
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Costmap ("each of the output maps get some     */
+/* weight assigned to them and the resulting per pixel sum is the cost in   */
+/* that pixel").  Reading B5: a layer that is NaN (undefined) contributes 0; */
+/* w[6] weights "unknown" (height undefined and not a negative obstacle).   */
+/* Accumulated in float32 in the order hard, soft, density, negative,       */
+/* slope, roughness, unknown.                                               */
+/* ------------------------------------------------------------------------ */
+void or_costmap(int64_t cells, const float w[7], const float* height, const float* density,
+                const uint8_t* hard, const uint8_t* soft, const uint8_t* neg, const float* slope,
+                const float* rough, float* cost) {
+  for (int64_t c = 0; c < cells; ++c) {
+    float acc = 0.0f;
+    acc = acc + w[0] * (float)hard[c];
+    acc = acc + w[1] * (float)soft[c];
+    acc = acc + w[2] * (isnan(density[c]) ? 0.0f : density[c]);
+    acc = acc + w[3] * (float)neg[c];
+    acc = acc + w[4] * (isnan(slope[c]) ? 0.0f : slope[c]);
+    acc = acc + w[5] * (isnan(rough[c]) ? 0.0f : rough[c]);
+    acc = acc + w[6] * ((isnan(height[c]) && !neg[c]) ? 1.0f : 0.0f);
+    cost[c] = acc;
+  }
+}

@@ -69,6 +69,7 @@ def lib():
                                     P, P, P, P, P, P]
         _lib.or_slope_roughness.argtypes = [i32, i32, f64, i32, i32, P, P, P, P]
         _lib.or_negative.argtypes = [i32, i32, i32, i64, P, P, P]
+        _lib.or_costmap.argtypes = [i64, P, P, P, P, P, P, P, P, P]
     return _lib
 
 
@@ -268,6 +269,18 @@ def negative(qs, defined, K, T_neg):
     lib().or_negative(nx, ny, K, int(T_neg), _p(np.ascontiguousarray(qs, dtype=np.int32)),
                       _p(np.ascontiguousarray(defined, dtype=np.uint8)), _p(neg))
     return neg.reshape(ny, nx)
+
+
+def costmap(L: "Layers", weights) -> np.ndarray:
+    """NEXT-4 costmap: weighted per-pixel sum of the layers (reading B5)."""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float32).reshape(7))
+    shp = L.height.shape
+    out = np.zeros(shp, dtype=np.float32)
+    c = lambda a, dt: np.ascontiguousarray(a, dtype=dt)  # noqa: E731
+    lib().or_costmap(out.size, _p(w), _p(c(L.height, np.float32)), _p(c(L.density, np.float32)),
+                     _p(c(L.hard, np.uint8)), _p(c(L.soft, np.uint8)), _p(c(L.neg, np.uint8)),
+                     _p(c(L.slope, np.float32)), _p(c(L.roughness, np.float32)), _p(out))
+    return out
 
 
 # --------------------------------------------------------------------------

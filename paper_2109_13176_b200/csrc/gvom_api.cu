@@ -91,8 +91,8 @@ Layout make_layout(const gvom_config* c) {
   l.tilecnt = off;  // per finalize tile: occupancy counts, offsets; then the done counter
   l.tilecnt_bytes = align_up(4 * (size_t)(2 * n_tiles(d) + 4));
   off += l.tilecnt_bytes;
-  l.layers_f32 = off;  // height, density, slope, rough
-  off += 4 * align_up(4 * (size_t)l.cells);
+  l.layers_f32 = off;  // height, density, slope, rough, cost
+  off += 5 * align_up(4 * (size_t)l.cells);
   l.layers_u8 = off;  // hard, soft, neg
   off += 3 * align_up((size_t)l.cells);
   l.qs = off;
@@ -337,6 +337,7 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.density = (float*)(h->ws + lay.layers_f32 + f32);
   h->layers.slope = (float*)(h->ws + lay.layers_f32 + 2 * f32);
   h->layers.rough = (float*)(h->ws + lay.layers_f32 + 3 * f32);
+  h->layers.cost = (float*)(h->ws + lay.layers_f32 + 4 * f32);
   h->layers.hard = (uint8_t*)(h->ws + lay.layers_u8);
   h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
   h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
@@ -643,6 +644,26 @@ gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t d
   GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->ms());
   }));
+  return GVOM_OK;
+}
+
+gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst, size_t dst_bytes) {
+  if (!h || !weights || !dst) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  const size_t bytes = 4 * (size_t)h->lay.cells;
+  if (dst_bytes < bytes) return GVOM_E_SIZE;
+  CostWeights cw;
+  for (int i = 0; i < 7; ++i) {
+    if (!isfinite(weights[i])) return GVOM_E_INVALID;
+    cw.w[i] = weights[i];
+  }
+  const bool direct = is_device_ptr(dst) && ((uintptr_t)dst & 3) == 0;
+  float* out = direct ? (float*)dst : h->layers.cost;
+  GVOM_CU(stage(
+      h, GVOM_STAGE_EXPORT, true,
+      [&] { return launch_costmap(h->d, h->layers, cw, out, h->ms()); }, h->ms()));
+  if (!direct)
+    GVOM_CU(cudaMemcpyAsync(dst, out, bytes, cudaMemcpyDefault, h->ms()));
   return GVOM_OK;
 }
 

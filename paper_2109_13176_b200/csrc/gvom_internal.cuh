@@ -53,6 +53,7 @@ struct LayerPtrs {
   uint8_t* neg;
   float* slope;
   float* rough;
+  float* cost;    // costmap scratch (gvom_costmap, NEXT-4)
   int32_t* qs;    // [ny][nx] fixed-point surface q_s, kQsUndef if undefined
   int32_t* qsT;   // [nx][ny] transposed copy (cone sweeps along x read it by line)
   int32_t* nmin;  // [ny][nx] min / max of the heights found by the cone search
@@ -152,6 +153,11 @@ struct CopyJob {
   int64_t bytes[GVOM_LAYER_COUNT];
 };
 cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st);
+struct CostWeights {
+  float w[7];  // hard, soft, density, negative, slope, roughness, unknown
+};
+cudaError_t launch_costmap(const Dims& d, const LayerPtrs& in, const CostWeights& cw, float* out,
+                           cudaStream_t st);
 
 inline int64_t rank_blocks(const Dims& d) {
   return (d.W + kRankWordsPerBlock - 1) / kRankWordsPerBlock;

@@ -482,6 +482,27 @@ __global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerPar
                    : 0;
 }
 
+// Costmap: weighted per-pixel sum of the layers,
+// f32 RN in the order hard, soft, density, negative, slope, roughness,
+// unknown; an undefined (NaN) layer contributes 0 (reading B5).
+__global__ void __launch_bounds__(256) k_costmap(const Dims d, const LayerPtrs in,
+                                                 const CostWeights cw, float* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)d.nx * d.ny) return;
+  const float h = __ldg(in.height + c), de = __ldg(in.density + c);
+  const float sl = __ldg(in.slope + c), ro = __ldg(in.rough + c);
+  const uint8_t ng = __ldg(in.neg + c);
+  float acc = 0.0f;
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[0], (float)__ldg(in.hard + c)));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[1], (float)__ldg(in.soft + c)));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[2], isnan(de) ? 0.0f : de));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[3], (float)ng));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[4], isnan(sl) ? 0.0f : sl));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[5], isnan(ro) ? 0.0f : ro));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[6], (isnan(h) && !ng) ? 1.0f : 0.0f));
+  out[c] = acc;
+}
+
 // merged occupancy bits of the combined map (export path)
 __global__ void __launch_bounds__(128) k_merge_bits(const SlotSet ss, const Dims d,
                                                     uint32_t* __restrict__ mbits) {
@@ -628,6 +649,12 @@ cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st) {
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 4) blocks = 148 * 4;
   k_export_layers<<<dim3((unsigned)blocks, GVOM_LAYER_COUNT), 256, 0, st>>>(job);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_costmap(const Dims& d, const LayerPtrs& in, const CostWeights& cw, float* out,
+                           cudaStream_t st) {
+  k_costmap<<<cells_blocks(d, 256), 256, 0, st>>>(d, in, cw, out);
   return cudaGetLastError();
 }
 

@@ -102,6 +102,7 @@ def load_library() -> C.CDLL:
         "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
         "gvom_surface_buffer": ([P, P], I32),
         "gvom_map_stream": ([P, P], I32),
+        "gvom_costmap": ([P, P, P, C.c_size_t], I32),
         "gvom_abi_version": ([], I32),
     }
     for name, (args, res) in sig.items():
@@ -117,7 +118,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_export_2d", "gvom_export_layers", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
-            "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream")
+            "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -326,6 +327,16 @@ class GvomMap:
         sizes = (C.c_size_t * 7)(*[res[n].numel() * res[n].element_size() for n in LAYERS])
         _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
         return res
+
+    def costmap(self, weights, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Weighted per-pixel sum of the layers; weights = (hard, soft,
+        density, negative, slope, roughness, unknown)."""
+        w = (C.c_float * 7)(*[float(v) for v in weights])
+        if out is None:
+            out = torch.empty((self.ny, self.nx), dtype=torch.float32, device=self.device)
+        _check(self.lib.gvom_costmap(self.h, w, C.c_void_p(out.data_ptr()),
+                                     out.numel() * out.element_size()), "gvom_costmap")
+        return out
 
     def map_origin(self) -> np.ndarray:
         o = (C.c_int64 * 3)()

@@ -195,3 +195,26 @@ def test_pipelined_mode_overlapping_frames(speed):
     for got, ref in zip(outs, refs):
         compare_layers({k: v.cpu().numpy() for k, v in got.items()}, ref)
     compare_merged(m, om)
+
+
+def test_costmap_matches_oracle(c2):
+    f = c2.frames[0]
+    m = GvomMap(c2.grid, max_points_per_frame=f.n_points)
+    om = O.OracleMap(c2.grid)
+    m.shift(f.vehicle_xyz)
+    om.shift(f.vehicle_xyz)
+    m.integrate_scan([to_dev(s) for s in f.scans])
+    om.integrate([(s.points, s.pose) for s in f.scans])
+    m.compute_maps()
+    L = om.compute_maps()
+    rs = np.random.default_rng(1)
+    for _ in range(3):
+        w = rs.uniform(0.0, 10.0, 7).astype(np.float32)
+        got = m.costmap(w)
+        host = torch.empty_like(got, device="cpu").pin_memory()
+        m.costmap(w, host)  # host destination path
+        m.synchronize()
+        ref = O.costmap(L, w)
+        tol = 1e-4 * (1.0 + float(np.abs(w).sum()))
+        assert np.allclose(got.cpu().numpy(), ref, rtol=1e-5, atol=tol)
+        assert np.array_equal(got.cpu().numpy(), host.numpy())
