@@ -295,7 +295,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2109_13176_b200 import GvomMap
+    from paper_2109_13176_b200 import GvomMap, LAYERS
     w = load_workload(args.config, args.frames, rank)
     frames = w.frames
     npts = w.points_per_frame
@@ -305,7 +305,7 @@ def main():
                   for f in frames]
     out = {k: torch.empty((m.ny, m.nx), dtype=(torch.uint8 if k in ("hard", "soft", "neg")
                                                else torch.float32), device=dev)
-           for k in ("height", "density", "hard", "soft", "neg", "slope", "roughness")}
+           for k in LAYERS}
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
@@ -443,7 +443,7 @@ def main():
             "config": {"workload": w.name, "points_per_scan": npts, "sensors": scans_per_frame,
                        "grid": f"{m.nx}x{m.ny}x{m.nz}@{w.grid['res']}m", "buffer_frames": K,
                        "frames_cycled": len(frames), "l2": "flushed (256 MiB write) between steps",
-                       "step": "shift+integrate_scan+compute_maps+export_2d x7"},
+                       "step": "shift+integrate_scan+compute_maps+export of all 8 layers"},
             "map_updates_per_s": world * args.steps / (total_ms / 1e3),
             "roofline": {"bound": "hbm", "kernel": "k_raycast", "achieved": ray_gbs,
                          "peak": peak, "unit": "GB/s", "frac": ray_gbs / peak, "traffic": None,
@@ -457,7 +457,7 @@ def main():
             "stages_ms_per_step": {s: v[0] / n_inst for s, v in stage_all.items() if v[1]},
             "stages_note": "separate instrumented pass (events around every launch)",
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * npts,
-                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 4 + 3), "steps": e2e_steps},
+                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 5 + 3), "steps": e2e_steps},
             "pipelined": {"value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
                           "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),
                           "note": "GVOM_FLAG_PIPELINE: integrate(t+1) overlaps compute_maps(t); "

@@ -63,6 +63,9 @@ typedef enum gvom_status {
  * slot an integrate overwrites is fenced on the compute_maps that last read
  * it.  Results of compute_maps / exports are ordered on the map stream.      */
 #define GVOM_FLAG_PIPELINE 1
+/* SPEC S:338 / SURVEY 8(f) NEXT-3 variant: hard and soft obstacle cells are
+ * left out of every slope / roughness window (and get NaN themselves).    */
+#define GVOM_FLAG_SLOPE_SKIP_OBSTACLES 2
 
 typedef struct gvom_config {
   int32_t nx, ny, nz;            /* voxels, each >= 1, nz <= 2048, nx*ny*nz < 2^31 */
@@ -121,7 +124,9 @@ typedef enum gvom_layer {
   GVOM_LAYER_NEGATIVE = 4,  /* u8 negative obstacle              */
   GVOM_LAYER_SLOPE = 5,     /* f32 radians, atan |grad| of the plane    */
   GVOM_LAYER_ROUGHNESS = 6, /* f32 m^2, mean squared plane residual     */
-  GVOM_LAYER_COUNT = 7
+  GVOM_LAYER_SPREAD = 7,    /* f32 m^2, variance of the returns in the surface
+                               voxel from the moments m1, m2 (NEXT-3, A13)     */
+  GVOM_LAYER_COUNT = 8
 } gvom_layer;
 
 typedef struct gvom_handle gvom_handle;
@@ -166,8 +171,8 @@ GVOM_API gvom_status gvom_compute_maps(gvom_handle* h);
  * GVOM_E_SIZE.  Stream-ordered: synchronise before reading a host dst.     */
 GVOM_API gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes);
 
-/* All seven layers at once ("each of these maps are published"):
- * dst[l] / dst_bytes[l] for l = GVOM_LAYER_HEIGHT..GVOM_LAYER_ROUGHNESS, each
+/* All layers at once ("each of these maps are published"):
+ * dst[l] / dst_bytes[l] for l = GVOM_LAYER_HEIGHT..GVOM_LAYER_SPREAD, each
  * as in gvom_export_2d.  When every dst is 16-byte aligned device memory the
  * copy is one kernel launch; otherwise one async copy per layer.           */
 GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],

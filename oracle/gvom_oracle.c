@@ -366,9 +366,16 @@ static int64_t or_det3(int64_t a, int64_t b, int64_t c, int64_t d, int64_t e, in
   return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
 }
 
+/* exclude (NULL = none): cells excluded from every window and given NaN
+ * themselves -- the NEXT-3 variant "excluding obstacle cells from slope
+ * windows", with exclude = hard | soft.                      */
 void or_slope_roughness(int32_t nx, int32_t ny, double res, int32_t N, int32_t min_pts,
-                        const int32_t* qs, const uint8_t* defined, float* slope, float* rough) {
+                        const int32_t* qs, const uint8_t* defined_in, const uint8_t* exclude,
+                        float* slope, float* rough) {
   int32_t r = (N - 1) / 2;
+  uint8_t* defined = (uint8_t*)malloc((size_t)nx * ny);
+  for (int64_t c = 0; c < (int64_t)nx * ny; ++c)
+    defined[c] = defined_in[c] && !(exclude && exclude[c]);
   for (int64_t y = 0; y < ny; ++y)
     for (int64_t x = 0; x < nx; ++x) {
       int64_t c = x + (int64_t)nx * y;
@@ -417,6 +424,33 @@ void or_slope_roughness(int32_t nx, int32_t ny, double res, int32_t N, int32_t m
         }
       double sc = res / 65536.0;
       rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
+    }
+  free(defined);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Point spread (BASELINE north_star "the spread of     */
+/* points about that surface"; moments m1, m2 of reading A13): variance of  */
+/* the return heights inside each column's surface voxel z*, in m^2:        */
+/*   (H*M2 - M1^2) / H^2 * (res/65536)^2, numerator an exact integer.       */
+/* NaN where the height is undefined.                                       */
+/* ------------------------------------------------------------------------ */
+void or_spread(int32_t nx, int32_t ny, int32_t nz, double res, const uint64_t* H,
+               const uint64_t* M1, const uint64_t* M2, float* spread) {
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) {
+      int64_t c = x + (int64_t)nx * y;
+      spread[c] = NAN;
+      for (int64_t z = 0; z < nz; ++z) {
+        int64_t L = or_lin(x, y, z, nx, nz);
+        if (H[L] < 1) continue;
+        unsigned __int128 num = (unsigned __int128)H[L] * M2[L] -
+                                (unsigned __int128)M1[L] * M1[L];
+        double h = (double)H[L];
+        double sc = res / 65536.0;
+        spread[c] = (float)((double)num / (h * h) * (sc * sc));
+        break;
+      }
     }
 }
 

@@ -67,7 +67,8 @@ def lib():
         _lib.or_combine.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, P, P]
         _lib.or_columns.argtypes = [i32, i32, i32, f64, i64, i64, i64, i64, P, P, P,
                                     P, P, P, P, P, P]
-        _lib.or_slope_roughness.argtypes = [i32, i32, f64, i32, i32, P, P, P, P]
+        _lib.or_slope_roughness.argtypes = [i32, i32, f64, i32, i32, P, P, P, P, P]
+        _lib.or_spread.argtypes = [i32, i32, i32, f64, P, P, P, P]
         _lib.or_negative.argtypes = [i32, i32, i32, i64, P, P, P]
         _lib.or_costmap.argtypes = [i64, P, P, P, P, P, P, P, P, P]
     return _lib
@@ -198,6 +199,7 @@ class Layers:
     roughness: np.ndarray
     qs: np.ndarray
     defined: np.ndarray
+    spread: Optional[np.ndarray] = None
 
 
 def combine(dims, slots: Sequence[FrameMap], o):
@@ -252,14 +254,24 @@ def columns(dims, res, o_z, T, H, Mi, mn):
             qs.reshape(sh), defined.reshape(sh))
 
 
-def slope_roughness(qs, defined, res, N, min_pts):
-    """O9 on [ny, nx] fixed-point heights."""
+def slope_roughness(qs, defined, res, N, min_pts, exclude=None):
+    """O9 on [ny, nx] fixed-point heights (exclude: cells left out, NEXT-3)."""
     ny, nx = qs.shape
     sl = np.zeros(nx * ny, dtype=np.float32)
     ro = np.zeros(nx * ny, dtype=np.float32)
+    ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.uint8)
     lib().or_slope_roughness(nx, ny, res, N, min_pts, _p(np.ascontiguousarray(qs, dtype=np.int32)),
-                             _p(np.ascontiguousarray(defined, dtype=np.uint8)), _p(sl), _p(ro))
+                             _p(np.ascontiguousarray(defined, dtype=np.uint8)),
+                             None if ex is None else _p(ex), _p(sl), _p(ro))
     return sl.reshape(ny, nx), ro.reshape(ny, nx)
+
+
+def spread(dims, res, H, M1, M2):
+    """NEXT-3 point spread of the surface voxel, [ny, nx] f32 m^2."""
+    nx, ny, nz = dims
+    out = np.zeros(nx * ny, dtype=np.float32)
+    lib().or_spread(nx, ny, nz, res, _p(H), _p(M1), _p(M2), _p(out))
+    return out.reshape(ny, nx)
 
 
 def negative(qs, defined, K, T_neg):
@@ -336,13 +348,15 @@ class OracleMap:
         height, dens, hard, soft, qs, dfn = columns(self.dims, self.res, o[2], self.T, H, Mi, mn)
         self._t("columns", t0)
         t0 = time.perf_counter()
+        ex = (hard | soft) if self.g.get("slope_skip_obstacles", False) else None
         sl, ro = slope_roughness(qs, dfn, self.res, int(self.g["slope_window"]),
-                                 int(self.g["min_plane_points"]))
+                                 int(self.g["min_plane_points"]), ex)
         self._t("slope_roughness", t0)
         t0 = time.perf_counter()
         neg = negative(qs, dfn, int(self.g["neg_obs_search_cells"]), self.T[3])
         self._t("negative", t0)
-        return Layers(height, dens, hard, soft, neg, sl, ro, qs, dfn)
+        spr = spread(self.dims, self.res, H, M1, M2)
+        return Layers(height, dens, hard, soft, neg, sl, ro, qs, dfn, spr)
 
     def merged_map(self) -> FrameMap:
         """The combined voxel map encoded as LUT + data (O7 + O6)."""

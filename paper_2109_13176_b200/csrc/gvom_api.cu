@@ -50,7 +50,7 @@ bool valid_config(const gvom_config* c) {
   if (c->slope_window < 3 || c->slope_window > 9 || (c->slope_window % 2) == 0) return false;
   if (c->min_plane_points < 3) return false;
   if (!(c->neg_obs_threshold >= 0) || c->neg_obs_search_cells < 1) return false;
-  if (c->flags & ~GVOM_FLAG_PIPELINE) return false;
+  if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES)) return false;
   return true;
 }
 
@@ -91,8 +91,8 @@ Layout make_layout(const gvom_config* c) {
   l.tilecnt = off;  // per finalize tile: occupancy counts, offsets; then the done counter
   l.tilecnt_bytes = align_up(4 * (size_t)(2 * n_tiles(d) + 4));
   off += l.tilecnt_bytes;
-  l.layers_f32 = off;  // height, density, slope, rough, cost
-  off += 5 * align_up(4 * (size_t)l.cells);
+  l.layers_f32 = off;  // height, density, slope, rough, cost, spread
+  off += 6 * align_up(4 * (size_t)l.cells);
   l.layers_u8 = off;  // hard, soft, neg
   off += 3 * align_up((size_t)l.cells);
   l.qs = off;
@@ -338,6 +338,7 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.slope = (float*)(h->ws + lay.layers_f32 + 2 * f32);
   h->layers.rough = (float*)(h->ws + lay.layers_f32 + 3 * f32);
   h->layers.cost = (float*)(h->ws + lay.layers_f32 + 4 * f32);
+  h->layers.spread = (float*)(h->ws + lay.layers_f32 + 5 * f32);
   h->layers.hard = (uint8_t*)(h->ws + lay.layers_u8);
   h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
   h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
@@ -359,6 +360,7 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.slope_window = cfg->slope_window;
   h->lp.min_plane_points = cfg->min_plane_points;
   h->lp.neg_cells = cfg->neg_obs_search_cells;
+  h->lp.skip_obstacles = (cfg->flags & GVOM_FLAG_SLOPE_SKIP_OBSTACLES) ? 1 : 0;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
   bool ok = true;
@@ -600,6 +602,7 @@ static const void* layer_src(gvom_handle* h, int layer, size_t* elem) {
     case GVOM_LAYER_HARD: *elem = 1; return h->layers.hard;
     case GVOM_LAYER_SOFT: *elem = 1; return h->layers.soft;
     case GVOM_LAYER_NEGATIVE: *elem = 1; return h->layers.neg;
+    case GVOM_LAYER_SPREAD: return h->layers.spread;
     default: return nullptr;
   }
 }

@@ -54,6 +54,7 @@ struct LayerPtrs {
   float* slope;
   float* rough;
   float* cost;    // costmap scratch (gvom_costmap, NEXT-4)
+  float* spread;  // variance of the surface voxel's returns (NEXT-3)
   int32_t* qs;    // [ny][nx] fixed-point surface q_s, kQsUndef if undefined
   int32_t* qsT;   // [nx][ny] transposed copy (cone sweeps along x read it by line)
   int32_t* nmin;  // [ny][nx] min / max of the heights found by the cone search
@@ -65,6 +66,7 @@ struct LayerParams {
   double res;
   int64_t o_z;
   int32_t slope_window, min_plane_points, neg_cells;
+  int32_t skip_obstacles;  // GVOM_FLAG_SLOPE_SKIP_OBSTACLES
 };
 
 // ---- launchers (each launches exactly one kernel; returns cudaError_t) ----

@@ -136,6 +136,20 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   // ---- the surface voxel ----
   const SlotVox v0 = slot_vox(col && zs >= 0, lut, data, cb, zs + dz, d.nz);
   const uint32_t mn0 = grp_min(v0.mn, lg);
+  // moments of the surface voxel (point spread, NEXT-3)
+  uint64_t sh = 0, s1 = 0, s2 = 0;
+  if (col && zs >= 0 && (unsigned)(zs + dz) < (unsigned)d.nz) {
+    const int32_t r0 = __ldg(lut + cb + zs + dz);
+    if (r0 >= 0) {
+      const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(data + r0) + 1);
+      sh = v0.h;
+      s1 = mm.x;
+      s2 = mm.y;
+    }
+  }
+  sh = grp_add64(sh, lg);
+  s1 = grp_add64(s1, lg);
+  s2 = grp_add64(s2, lg);
   const int64_t q_s = 65536ll * zs + (int64_t)mn0;
   const int z_lo = (int)((q_s + lp.T_lo) >> 16);
   const int64_t zh = (q_s + lp.T_hi) >> 16;
@@ -193,7 +207,13 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   if (zs < 0) {
     out.height[c] = __int_as_float(0x7fc00000);
     out.density[c] = __int_as_float(0x7fc00000);
+    out.spread[c] = __int_as_float(0x7fc00000);
     return;
+  }
+  {
+    const unsigned __int128 num = (unsigned __int128)sh * s2 - (unsigned __int128)s1 * s1;
+    const double hh = (double)sh, sc = lp.res / 65536.0;
+    out.spread[c] = (float)((double)num / (hh * hh) * (sc * sc));
   }
   out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
   if (SH == 0) {
@@ -227,9 +247,13 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   for (int i = threadIdx.y * kSlopeTX + threadIdx.x; i < SW_ * SH_; i += kSlopeTX * kSlopeTY) {
     const int ty = i / SW_, tx = i % SW_;
     const int gx = x0 + tx - kSlopeHalo, gy = y0 + ty - kSlopeHalo;
-    tile[ty][tx] = ((unsigned)gx < (unsigned)d.nx && (unsigned)gy < (unsigned)d.ny)
-                       ? __ldg(qs + gx + (int64_t)d.nx * gy)
-                       : kQsUndef;
+    int32_t q = kQsUndef;
+    if ((unsigned)gx < (unsigned)d.nx && (unsigned)gy < (unsigned)d.ny) {
+      const int64_t cc = gx + (int64_t)d.nx * gy;
+      q = __ldg(qs + cc);
+      if (lp.skip_obstacles && (__ldg(out.hard + cc) | __ldg(out.soft + cc))) q = kQsUndef;
+    }
+    tile[ty][tx] = q;
   }
   __syncthreads();
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;

@@ -22,8 +22,9 @@ import torch
 
 from . import build_ext
 
-LAYERS = ("height", "density", "hard", "soft", "neg", "slope", "roughness")
-LAYER_ID = {"height": 0, "density": 1, "hard": 2, "soft": 3, "neg": 4, "slope": 5, "roughness": 6}
+LAYERS = ("height", "density", "hard", "soft", "neg", "slope", "roughness", "spread")
+LAYER_ID = {"height": 0, "density": 1, "hard": 2, "soft": 3, "neg": 4, "slope": 5, "roughness": 6,
+            "spread": 7}
 LAYER_U8 = {"hard", "soft", "neg"}
 STAGES = ("raycast", "rank_count", "rank_scan", "finalize", "endpoint", "columns", "slope",
           "negative", "memset", "h2d", "export", "merge")
@@ -127,7 +128,8 @@ def make_config(grid: dict, max_points_per_frame: int) -> Config:
     c.res = float(grid["res"])
     c.z_center_frac = float(grid.get("z_center_frac", 0.5))
     c.buffer_frames = int(grid.get("buffer_frames", 8))
-    c.flags = 1 if grid.get("pipeline", False) else 0  # GVOM_FLAG_PIPELINE
+    c.flags = (1 if grid.get("pipeline", False) else 0) | (  # GVOM_FLAG_PIPELINE
+        2 if grid.get("slope_skip_obstacles", False) else 0)  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES
     c.max_points_per_frame = int(max_points_per_frame)
     c.min_obstacle_height = float(grid["min_obstacle_height"])
     c.max_obstacle_height = float(grid["max_obstacle_height"])
@@ -323,8 +325,9 @@ class GvomMap:
                 t = torch.empty((self.ny, self.nx), dtype=dt, device=self.device)
             assert t.is_contiguous()
             res[name] = t
-        ptrs = (C.c_void_p * 7)(*[res[n].data_ptr() for n in LAYERS])
-        sizes = (C.c_size_t * 7)(*[res[n].numel() * res[n].element_size() for n in LAYERS])
+        ptrs = (C.c_void_p * len(LAYERS))(*[res[n].data_ptr() for n in LAYERS])
+        sizes = (C.c_size_t * len(LAYERS))(*[res[n].numel() * res[n].element_size()
+                                             for n in LAYERS])
         _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
         return res
 

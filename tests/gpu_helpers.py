@@ -43,8 +43,11 @@ def compare_layers(got: dict, L: "O.Layers"):
         g = got[k]
         bad = np.argwhere(g != ref)
         assert bad.size == 0, f"{k} mismatch at {len(bad)} cells, first {bad[:5].tolist()}"
-    for k, ref in (("height", L.height), ("density", L.density), ("slope", L.slope),
-                   ("roughness", L.roughness)):
+    fl = [("height", L.height), ("density", L.density), ("slope", L.slope),
+          ("roughness", L.roughness)]
+    if L.spread is not None and "spread" in got:
+        fl.append(("spread", L.spread))
+    for k, ref in fl:
         g = got[k]
         assert np.array_equal(np.isnan(g), np.isnan(ref)), f"{k} nodata mask differs"
         ok = ~np.isnan(ref)

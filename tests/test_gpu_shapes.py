@@ -52,3 +52,11 @@ def test_shapes_and_parameters(case):
     w, frames = _world_frames(4, 0.37 + 0.1 * case, 100 + case)
     wl = synth.Workload(f"shape{case}", grid, frames, w)
     run_sequence(wl, check_every=1)
+
+
+def test_slope_skip_obstacles_flag():
+    # GVOM_FLAG_SLOPE_SKIP_OBSTACLES (SPEC S:338 variant) against the oracle
+    grid = synth.grid_cfg(64, 64, 24, 0.25, buffer_frames=2)
+    grid["slope_skip_obstacles"] = True
+    w, frames = _world_frames(3, 0.3, 77)
+    run_sequence(synth.Workload("skip_obstacles", grid, frames, w))

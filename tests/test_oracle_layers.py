@@ -327,3 +327,38 @@ def test_negative_monotone_in_threshold():
             assert np.all(neg <= prev)
         prev = neg
     assert prev.sum() == 0
+
+
+# ------------------------------------------------------------ NEXT-3 variants
+def test_spread_closed_form():
+    # point spread of the surface voxel = population variance of its return
+    # heights (numpy.var of the fixed-point values), times (res/65536)^2
+    res = 0.25
+    rs = np.random.default_rng(5)
+    for n in (1, 2, 5, 40):
+        dz = rs.integers(0, 65536, size=n).astype(np.uint64)
+        nz = 6
+        H = np.zeros(nz, np.uint64)
+        M1 = np.zeros(nz, np.uint64)
+        M2 = np.zeros(nz, np.uint64)
+        H[2], M1[2], M2[2] = n, dz.sum(), (dz * dz).sum()
+        H[4], M1[4], M2[4] = 3, 10, 1000  # a higher voxel is ignored
+        sp = O.spread((1, 1, nz), res, H, M1, M2)[0, 0]
+        exp = np.var(dz.astype(np.float64)) * (res / 65536) ** 2
+        assert sp == pytest.approx(exp, rel=1e-6, abs=1e-15)
+    assert math.isnan(O.spread((1, 1, 3), res, np.zeros(3, np.uint64), np.zeros(3, np.uint64),
+                               np.zeros(3, np.uint64))[0, 0])
+
+
+def test_slope_excluding_obstacle_cells():
+    # SPEC S:338 variant: excluded cells leave every window and get NaN
+    rs = np.random.default_rng(6)
+    q = rs.integers(0, 2 ** 20, size=(12, 12)).astype(np.int32)
+    dfn = np.ones((12, 12), np.uint8)
+    ex = (rs.random((12, 12)) < 0.2).astype(np.uint8)
+    sl, ro = O.slope_roughness(q, dfn, 0.25, 5, 4, ex)
+    sl2, ro2 = O.slope_roughness(q, (dfn & (1 - ex)).astype(np.uint8), 0.25, 5, 4)
+    assert np.array_equal(np.isnan(sl), np.isnan(sl2))
+    m = ~np.isnan(sl)
+    assert np.array_equal(sl[m], sl2[m]) and np.array_equal(ro[m], ro2[m])
+    assert np.all(np.isnan(sl[ex == 1]))
