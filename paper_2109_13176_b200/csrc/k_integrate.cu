@@ -160,34 +160,97 @@ __device__ void scan_tiles_if_last(const TileCounts& tc, const Dims& d) {
   }
 }
 
-// One miss increment per active lane at voxel L, merged across lanes that
-// hold the same voxel: one red.add per group (runs of adjacent lanes, or
-// arbitrary groups via match.any).
-template <bool kMatchAgg>
-__device__ __forceinline__ void aggregate_red(uint32_t* __restrict__ miss, uint32_t L, bool active,
-                                              unsigned act, unsigned after_lanes, int lane) {
-  const uint32_t key = active ? L : 0xffffffffu;
-  bool head;
-  uint32_t cnt;
-  if (kMatchAgg) {
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    head = active && lane == __ffs(peers) - 1;
-    cnt = (uint32_t)__popc(peers);
-  } else {
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-    head = active && (lane == 0 || prev != key);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
-  }
+// Miss increments of one warp step, merged over runs of adjacent lanes that
+// hold the same voxel: one red.add per run, issued by its first lane.  Two
+// schedules, chosen per launch by the miss grid's size (launch_raycast):
+//  - resident (kStream = false; the grid fits in L2): L is a 32-bit BYTE offset
+//    and an inactive lane carries the key ~0, which breaks runs by itself, so
+//    the step needs no mask of active lanes and runs on a warp-uniform trip
+//    count (fewest instructions per step);
+//  - streaming (kStream = true; REDs go out to HBM): L is the voxel index and
+//    the run count masks the inactive lanes; this schedule measured faster
+//    when the REDs are DRAM-latency bound (c5: 2.88 vs 3.08 ms), the resident
+//    one faster when they hit L2 (c2: 50 vs 55 us) -- see DESIGN.md.
+template <bool kStream>
+__device__ __forceinline__ uint32_t* miss_at(uint32_t* miss, uint32_t L) {
+  if (kStream) return miss + L;
+  return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(miss) + L);
+}
+
+__device__ __forceinline__ void red_run(uint32_t* addr, bool head, uint32_t cnt) {
   // no "memory" clobber: nothing in the kernel reads the miss grid, so the
   // reduction needs no ordering with the surrounding code
   asm volatile(
       "{ .reg .pred p; setp.ne.u32 p, %2, 0;\n\t"
-      "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(miss + L),
+      "@p red.relaxed.gpu.global.add.u32 [%0], %1; }" ::"l"(addr),
       "r"(cnt), "r"((uint32_t)head));
 }
 
-template <bool kMatchAgg, bool kAggFirst>
+// resident schedule: see above
+__device__ __forceinline__ void aggregate_red_resident(uint32_t* __restrict__ miss, uint32_t L,
+                                                       bool active, bool lane0,
+                                                       unsigned after_lanes, int lane) {
+  const uint32_t key = active ? L : 0xffffffffu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool brk = prev != key;
+  const unsigned heads = __ballot_sync(0xffffffffu, brk);
+  const bool head = active && (brk || lane0);
+  // run length = distance to the next run start above this lane (32 if none):
+  // ctz(x) = popc(~x & (x - 1)), which is 32 for x = 0 without a special case
+  asm volatile(
+      "{ .reg .pred p; .reg .b32 t, u;\n\t"
+      "and.b32 t, %1, %2;\n\t"
+      "add.u32 u, t, -1;\n\t"
+      "not.b32 t, t;\n\t"
+      "and.b32 t, t, u;\n\t"
+      "popc.b32 t, t;\n\t"
+      "sub.u32 t, t, %3;\n\t"
+      "setp.ne.u32 p, %4, 0;\n\t"
+      "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
+      "r"(heads), "r"(after_lanes), "r"(lane), "r"((uint32_t)head));
+}
+
+// streaming schedule: `act` = the warp's active lanes
+__device__ __forceinline__ void aggregate_red_stream(uint32_t* __restrict__ miss, uint32_t L,
+                                                     bool active, unsigned act,
+                                                     unsigned after_lanes, int lane) {
+  const uint32_t key = active ? L : 0xffffffffu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = active && (lane == 0 || prev != key);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
+  red_run(miss_at<true>(miss, L), head, cnt);
+}
+
+#ifndef GVOM_RAY_STREAM_BYTES
+#define GVOM_RAY_STREAM_BYTES (int64_t(64) << 20)
+#endif
+// miss grids above this size take the streaming schedule (B200 L2: 126 MB,
+// split over two dies; tuned on c4 / c5)
+constexpr int64_t kRayStreamBytes = GVOM_RAY_STREAM_BYTES;
+
+// One DDA step (O5): argmin of the three keys, strict <, ties to the lowest
+// axis; no gating needed: a lane past its walk keeps stepping unseen (its
+// exhausted axes carry +inf keys, see the setup in k_raycast).
+__device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float& e0, float& e1,
+                                         float& e2, float f0, float f1, float f2, float i0,
+                                         float i1, float i2, float s0, float s1, float s2,
+                                         int dL0, int dL1, int dL2, uint32_t& L) {
+  const bool l10 = k1 < k0;
+  const float b01 = l10 ? k1 : k0;
+  const bool u2 = k2 < b01;
+  const bool u1 = l10 && !u2;
+  const bool u0 = !l10 && !u2;
+  e0 = u0 ? __fadd_rn(e0, f0) : e0;
+  e1 = u1 ? __fadd_rn(e1, f1) : e1;
+  e2 = u2 ? __fadd_rn(e2, f2) : e2;
+  L += (uint32_t)(u2 ? dL2 : (u1 ? dL1 : dL0));
+  k0 = __fmul_rn(__fsub_rn(e0, s0), i0);
+  k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
+  k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
+}
+
+template <bool kStream>
 __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatch rb,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
@@ -307,10 +370,11 @@ __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatc
           k0 = rem[0] > 0 ? axis_key(eb[0], fb[0], s0, i0, 1) : kInf;
           k1 = rem[1] > 0 ? axis_key(eb[1], fb[1], s1, i1, 1) : kInf;
           k2 = rem[2] > 0 ? axis_key(eb[2], fb[2], s2, i2, 1) : kInf;
-          dL0 = st[0] * str[0];
-          dL1 = st[1] * str[1];
-          dL2 = st[2] * str[2];
-          L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]);
+          constexpr int unit = kStream ? 1 : 4;  // see miss_at
+          dL0 = st[0] * str[0] * unit;
+          dL1 = st[1] * str[1] * unit;
+          dL2 = st[2] * str[2] * unit;
+          L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]) * unit;
         }
       }
     }
@@ -323,28 +387,25 @@ __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatc
       atomicAdd(tc.tile + newtile, (uint32_t)__popc(peers));
   }
   const unsigned after_lanes = 0xfffffffeu << lane;  // lanes above this one
-  unsigned act = __ballot_sync(0xffffffffu, left > 0);
-  while (act) {
-    const bool active = left > 0;
-    const uint32_t Lc = L;  // this step's voxel
-    if (kAggFirst) aggregate_red<kMatchAgg>(miss, Lc, active, act, after_lanes, lane);
-    // DDA step: argmin, strict <, ties to the lowest axis (O5); no gating
-    // needed (see above)
-    const bool l10 = k1 < k0;
-    const float b01 = l10 ? k1 : k0;
-    const bool u2 = k2 < b01;
-    const bool u1 = l10 && !u2;
-    const bool u0 = !l10 && !u2;
-    e0 = u0 ? __fadd_rn(e0, f0) : e0;
-    e1 = u1 ? __fadd_rn(e1, f1) : e1;
-    e2 = u2 ? __fadd_rn(e2, f2) : e2;
-    L += (uint32_t)(u2 ? dL2 : (u1 ? dL1 : dL0));
-    k0 = __fmul_rn(__fsub_rn(e0, s0), i0);
-    k1 = __fmul_rn(__fsub_rn(e1, s1), i1);
-    k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
-    --left;
-    if (!kAggFirst) aggregate_red<kMatchAgg>(miss, Lc, active, act, after_lanes, lane);
-    act = __ballot_sync(0xffffffffu, left > 0);
+  if (kStream) {
+    unsigned act = __ballot_sync(0xffffffffu, left > 0);
+    while (act) {
+      const bool active = left > 0;
+      aggregate_red_stream(miss, L, active, act, after_lanes, lane);
+      dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
+      --left;
+      act = __ballot_sync(0xffffffffu, left > 0);
+    }
+  } else {
+    const bool lane0 = lane == 0;
+    // warp-uniform trip count: lane i is active for its first left_i steps
+    const int Tw = __reduce_max_sync(0xffffffffu, left);
+#pragma unroll 1
+    for (int it = 0; it < Tw; ++it) {
+      const bool active = it < left;
+      aggregate_red_resident(miss, L, active, lane0, after_lanes, lane);
+      dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
+    }
   }
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
@@ -800,8 +861,13 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   // the long (upward / horizontal) and short (ground) rings over the SMs
   constexpr int bs = 64;
   const int64_t blocks = (threads + bs - 1) / bs;
-  k_raycast<false, true><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc,
-                                                          last_launch);
+  // schedule by where the REDs land (see aggregate_red_*): the resident one
+  // also needs byte offsets < 2^32
+  const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
+  if (miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32))
+    k_raycast<false><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+  else
+    k_raycast<true><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   return cudaGetLastError();
 }
 

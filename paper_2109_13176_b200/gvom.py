@@ -66,7 +66,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return build_ext.LIB
+    # GVOM_LIBRARY: an alternative in-tree build (A/B timing of kernel variants)
+    return os.environ.get("GVOM_LIBRARY") or build_ext.LIB
 
 
 def load_library() -> C.CDLL:
