@@ -178,6 +178,26 @@ GVOM_API gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst,
 GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
                                         const size_t dst_bytes[GVOM_LAYER_COUNT]);
 
+/* One scan end to end: gvom_shift + gvom_integrate_scan + gvom_compute_maps
+ * (+ gvom_export_layers when dst != NULL), same arguments, results and
+ * errors as those calls in sequence (inputs are validated before anything is
+ * enqueued).  The frame's kernels are captured on the handle's stream and run
+ * as ONE CUDA graph launch: the cached executable graph is patched with the
+ * frame's arguments (cudaGraphExecUpdate) or re-instantiated when the launch
+ * topology changed.  Falls back to plain stream launches (same kernels) when
+ * capture does not apply: pipelined mode, points in pageable
+ * host memory, or the stream already under capture by the caller.  The
+ * graph and a private capture stream are driver objects held by the handle
+ * (released by gvom_destroy); no device memory is allocated.              */
+GVOM_API gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,
+                               int32_t n_scans, void* const dst[GVOM_LAYER_COUNT],
+                               const size_t dst_bytes[GVOM_LAYER_COUNT],
+                               int64_t out_delta_voxels[3]);
+
+/* gvom_step counters: out[0] graph launches, out[1] graph instantiations,
+ * out[2] steps run without a graph.                                        */
+GVOM_API gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]);
+
 /* Costmap ("each of the output maps get some weight assigned to them
  * and the resulting per pixel sum is the cost in that pixel"; SURVEY 8(f)
  * NEXT-4).  cost = w0*hard + w1*soft + w2*density + w3*negative + w4*slope

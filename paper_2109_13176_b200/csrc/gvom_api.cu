@@ -154,6 +154,11 @@ struct gvom_handle {
   cudaEvent_t ev_maps[kMapsRing] = {};
   int64_t maps_calls = 0;           // compute_maps calls so far
   std::vector<int64_t> slot_reader; // last compute_maps call that read a slot
+  // gvom_step: the frame's launches, captured and replayed as one CUDA graph
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap = nullptr;          // capture stream (the caller's may be legacy)
+  bool capturing = false;              // inside gvom_step's capture
+  int64_t graph_stats[3] = {0, 0, 0};  // graph launches, instantiations, eager steps
   cudaStream_t ms() const { return pipelined ? mst : st; }
 };
 
@@ -179,11 +184,12 @@ cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f, cudaStream_t on
   if (timed) {
     a = take_event(h);
     b = take_event(h);
-    if (a) cudaEventRecord(a, ts);
+    // under capture: external event-record nodes, recorded at every replay
+    if (a) cudaEventRecordWithFlags(a, ts, h->capturing ? cudaEventRecordExternal : 0u);
   }
   const cudaError_t e = f();
   if (timed && a && b) {
-    cudaEventRecord(b, ts);
+    cudaEventRecordWithFlags(b, ts, h->capturing ? cudaEventRecordExternal : 0u);
     h->recs.push_back({id, a, b});
   }
   if (is_kernel && e == cudaSuccess) h->launches++;
@@ -220,6 +226,15 @@ SensorParams sensor_params(const gvom_config& c, const double* P, const int64_t 
     sp.S[i] = (int32_t)floorf(sp.b[i]);
   }
   return sp;
+}
+
+bool is_pinned_host_ptr(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
 }
 
 bool is_device_ptr(const void* p) {
@@ -395,6 +410,8 @@ gvom_status gvom_destroy(gvom_handle* h) {
   for (auto e : h->ev_maps)
     if (e) cudaEventDestroy(e);
   if (h->mst) cudaStreamDestroy(h->mst);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->cap) cudaStreamDestroy(h->cap);
   delete h;
   return GVOM_OK;
 }
@@ -633,6 +650,96 @@ gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT]
                              h->ms());
     }, h->ms()));
   }
+  return GVOM_OK;
+}
+
+// One scan end to end (shift + integrate + compute_maps + export): the host
+// work is done first (inputs validated before anything is enqueued), then the
+// frame's launches are captured on the handle's stream, patched into the cached
+// executable graph (cudaGraphExecUpdate: same topology, new kernel arguments)
+// or instantiated anew, and launched as one graph.
+gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,
+                      int32_t n_scans, void* const dst[GVOM_LAYER_COUNT],
+                      const size_t dst_bytes[GVOM_LAYER_COUNT], int64_t out_delta[3]) {
+  if (!h || !vehicle_xyz) return GVOM_E_INVALID;
+  if (dst && !dst_bytes) return GVOM_E_INVALID;
+  if (dst)
+    for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
+      size_t elem;
+      layer_src(h, l, &elem);
+      if (!dst[l]) return GVOM_E_INVALID;
+      if (dst_bytes[l] < elem * (size_t)h->lay.cells) return GVOM_E_SIZE;
+    }
+  const gvom_status ss = gvom_shift(h, vehicle_xyz, out_delta);
+  if (ss != GVOM_OK) return ss;
+  {
+    SensorParams sp[GVOM_MAX_SENSORS];
+    const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
+    if (ps != GVOM_OK) return ps;
+  }
+  // capture needs stream-ordered work only: no cross-call events (pipelined
+  // mode), points on the device or in pinned host memory (stage-timing events
+  // become external event-record nodes, see stage()),
+  // and a stream that is not already being captured by the caller
+  bool graph = !h->pipelined;
+  for (int i = 0; graph && i < n_scans; ++i)
+    if (scans[i].n > 0 && !is_device_ptr(scans[i].xyzw) && !is_pinned_host_ptr(scans[i].xyzw))
+      graph = false;
+  if (graph) {
+    cudaStreamCaptureStatus cs;
+    GVOM_CU(cudaStreamIsCapturing(h->st, &cs));
+    graph = cs == cudaStreamCaptureStatusNone;
+  }
+  auto frame = [&]() -> gvom_status {
+    gvom_status s = gvom_integrate_scan(h, scans, n_scans);
+    if (s == GVOM_OK) s = gvom_compute_maps(h);
+    if (s == GVOM_OK && dst) s = gvom_export_layers(h, dst, dst_bytes);
+    return s;
+  };
+  if (!graph) {
+    h->graph_stats[2]++;
+    return frame();
+  }
+  // capture on the handle's private stream (the caller's stream may be the
+  // legacy default stream, which cannot be captured); the graph is then
+  // launched on the caller's stream
+  if (!h->cap) GVOM_CU(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+  cudaStream_t user = h->st;
+  GVOM_CU(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+  h->st = h->cap;
+  h->capturing = true;
+  const gvom_status fs = frame();
+  h->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(h->cap, &g);
+  h->st = user;
+  if (fs != GVOM_OK || ce != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return fs != GVOM_OK ? fs : GVOM_E_CUDA;
+  }
+  if (h->gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(h->gexec, g, &info) != cudaSuccess) {
+      cudaGetLastError();  // topology changed (e.g. an empty scan): instantiate anew
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!h->gexec) {
+    e = cudaGraphInstantiate(&h->gexec, g, 0);
+    if (e == cudaSuccess) h->graph_stats[1]++;
+  }
+  cudaGraphDestroy(g);
+  if (e == cudaSuccess) e = cudaGraphLaunch(h->gexec, user);
+  if (e != cudaSuccess) return GVOM_E_CUDA;
+  h->graph_stats[0]++;
+  return GVOM_OK;
+}
+
+gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]) {
+  if (!h || !out) return GVOM_E_INVALID;
+  for (int i = 0; i < 3; ++i) out[i] = h->graph_stats[i];
   return GVOM_OK;
 }
 

@@ -91,6 +91,8 @@ def load_library() -> C.CDLL:
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
         "gvom_export_layers": ([P, P, P], I32),
+        "gvom_step": ([P, P, P, I32, P, P, P], I32),
+        "gvom_graph_stats": ([P, P], I32),
         "gvom_map_origin": ([P, P], I32),
         "gvom_export_voxels": ([P, P, P, I64, P], I32),
         "gvom_export_frame": ([P, I32, P, P, I64, P, P], I32),
@@ -120,7 +122,8 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_export_2d", "gvom_export_layers", "gvom_map_origin", "gvom_export_voxels", "gvom_export_frame",
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
-            "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap")
+            "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
+            "gvom_step", "gvom_graph_stats")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -281,25 +284,8 @@ class GvomMap:
         """scans: (points, pose[3,4], rings).  points: float32 [n,4] torch tensor
         (cuda or pinned/pageable cpu) or numpy array; host points are copied by
         the library inside the call (stream-ordered)."""
-        items = list(scans)
-        arr = (Scan * max(1, len(items)))()
-        keep = []
-        for i, it in enumerate(items):
-            pts, pose = it[0], it[1]
-            rings = int(it[2]) if len(it) > 2 else 0
-            if isinstance(pts, np.ndarray):
-                pts = torch.from_numpy(np.ascontiguousarray(pts, dtype=np.float32))
-            if pts.dtype != torch.float32 or pts.dim() != 2 or pts.shape[1] != 4:
-                raise ValueError("points must be float32 [n, 4]")
-            pts = pts.contiguous()
-            keep.append(pts)
-            arr[i].xyzw = pts.data_ptr() if pts.numel() else None
-            arr[i].n = pts.shape[0]
-            P = np.ascontiguousarray(np.asarray(pose, dtype=np.float64).reshape(12))
-            for j in range(12):
-                arr[i].sensor_to_world[j] = float(P[j])
-            arr[i].rings = rings
-        rc = self.lib.gvom_integrate_scan(self.h, arr, len(items))
+        arr, n, keep = self._scan_array(scans)
+        rc = self.lib.gvom_integrate_scan(self.h, arr, n)
         _check(rc, "gvom_integrate_scan")
         self._keep.append(keep)  # host buffers must live until the stream passes
 
@@ -315,9 +301,7 @@ class GvomMap:
                                        out.numel() * out.element_size()), f"export_2d({layer})")
         return out
 
-    def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None) -> Dict[str, torch.Tensor]:
-        """All seven layers with one gvom_export_layers call (one kernel when
-        every destination is device memory)."""
+    def _layer_dst(self, out):
         res = {}
         for name in LAYERS:
             t = None if out is None else out[name]
@@ -329,8 +313,32 @@ class GvomMap:
         ptrs = (C.c_void_p * len(LAYERS))(*[res[n].data_ptr() for n in LAYERS])
         sizes = (C.c_size_t * len(LAYERS))(*[res[n].numel() * res[n].element_size()
                                              for n in LAYERS])
+        return res, ptrs, sizes
+
+    def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None) -> Dict[str, torch.Tensor]:
+        """All layers with one gvom_export_layers call (one kernel when every
+        destination is device memory)."""
+        res, ptrs, sizes = self._layer_dst(out)
         _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
         return res
+
+    def step(self, vehicle_xyz: Sequence[float], scans: Iterable[ScanLike],
+             out: Optional[Dict[str, torch.Tensor]] = None, export: bool = True):
+        """gvom_step: shift + integrate_scan + compute_maps (+ export of all
+        layers into `out`, allocated if None) as one CUDA graph launch.
+        Returns (shift delta, layers or None)."""
+        p = (C.c_double * 3)(*[float(v) for v in vehicle_xyz])
+        dlt = (C.c_int64 * 3)()
+        arr, n, keep = self._scan_array(scans)
+        res, ptrs, sizes = self._layer_dst(out) if export else (None, None, None)
+        _check(self.lib.gvom_step(self.h, p, arr, n, ptrs, sizes, dlt), "gvom_step")
+        self._keep.append(keep)
+        return np.array(dlt[:], dtype=np.int64), res
+
+    def graph_stats(self) -> dict:
+        o = (C.c_int64 * 3)()
+        _check(self.lib.gvom_graph_stats(self.h, o), "gvom_graph_stats")
+        return {"graph_launches": o[0], "instantiations": o[1], "eager_steps": o[2]}
 
     def costmap(self, weights, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Weighted per-pixel sum of the layers; weights = (hard, soft,

@@ -76,29 +76,37 @@ def layers_np(m: GvomMap) -> dict:
 
 
 def run_sequence(w, frames=None, *, host=False, check_every=1, check_merged=True,
-                 rings_override=None):
-    """Integrate frames on GPU and oracle; compare after every `check_every`."""
+                 rings_override=None, use_step=False):
+    """Integrate frames on GPU and oracle; compare after every `check_every`.
+    use_step: drive the GPU with gvom_step (one graph launch per frame)."""
     frames = w.frames if frames is None else frames
     npts = max(f.n_points for f in frames)
     m = GvomMap(w.grid, max_points_per_frame=max(npts, 1))
     om = O.OracleMap(w.grid)
     for i, f in enumerate(frames):
-        d_gpu = m.shift(f.vehicle_xyz)
-        d_ref = om.shift(f.vehicle_xyz)
-        assert np.array_equal(d_gpu, d_ref)
         scans = []
         for s in f.scans:
             pts, pose, rings = to_dev(s, host=host)
             if rings_override is not None:
                 rings = rings_override
             scans.append((pts, pose, rings))
-        m.integrate_scan(scans)
+        d_ref = om.shift(f.vehicle_xyz)
+        if use_step:
+            d_gpu, lay = m.step(f.vehicle_xyz, scans)
+        else:
+            d_gpu = m.shift(f.vehicle_xyz)
+            m.integrate_scan(scans)
+        assert np.array_equal(d_gpu, d_ref)
         fm = om.integrate([(s.points, s.pose) for s in f.scans])
         if (i + 1) % check_every == 0 or i == len(frames) - 1:
             compare_frame(m, fm)
-            m.compute_maps()
+            if not use_step:
+                m.compute_maps()
             L = om.compute_maps()
             assert np.array_equal(m.map_origin(), om.merged[5])
+            if use_step:
+                m.synchronize()
+                compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
             compare_layers(layers_np(m), L)
             if check_merged:
                 compare_merged(m, om)

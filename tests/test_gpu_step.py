@@ -1,0 +1,93 @@
+"""gvom_step (include/gvom.h): shift + integrate + compute_maps + export as one
+CUDA graph launch per frame must give exactly the results of the separate
+calls (parity against the oracle, frame by frame), patch the cached graph
+while the launch topology is unchanged, re-instantiate when it changes, and
+run the same kernels without a graph when capture does not apply."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2109_13176_b200 import GvomMap, SensorOutside, synth
+from tests.gpu_helpers import compare_layers, layers_np, run_sequence, to_dev
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_step_c2_matches_oracle():
+    m, _ = run_sequence(synth.workload(1), use_step=True)
+    st = m.graph_stats()
+    assert st["graph_launches"] == 1 and st["eager_steps"] == 0
+
+
+@pytest.mark.parametrize("speed", [4.5, 12.0])
+def test_step_motion_sequence_graph_updates(speed):
+    # shift + merge + eviction through the graph path; one instantiation,
+    # every later frame patches the cached graph with new arguments
+    w = synth.config3(speed=speed, n_frames=12, columns=1024)
+    m, _ = run_sequence(w, check_every=4, use_step=True)
+    st = m.graph_stats()
+    assert st["graph_launches"] == 12 and st["eager_steps"] == 0
+    assert st["instantiations"] == 1, st
+
+
+def test_step_c4_three_lidars():
+    m, _ = run_sequence(synth.workload(3), use_step=True)
+    assert m.graph_stats()["graph_launches"] == 1
+
+
+def test_step_pinned_host_points_use_graph():
+    m, _ = run_sequence(synth.workload(1), host=True, check_merged=False, use_step=True)
+    assert m.graph_stats()["graph_launches"] == 1
+
+
+def test_step_pageable_host_points_run_eagerly():
+    w = synth.workload(0)
+    f = w.frames[0]
+    m = GvomMap(w.grid, max_points_per_frame=f.n_points)
+    om = O.OracleMap(w.grid)
+    om.shift(f.vehicle_xyz)
+    om.integrate([(s.points, s.pose) for s in f.scans])
+    _, lay = m.step(f.vehicle_xyz, [(s.points, s.pose, s.rings) for s in f.scans])
+    m.synchronize()
+    compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, om.compute_maps())
+    st = m.graph_stats()
+    assert st["eager_steps"] == 1 and st["graph_launches"] == 0
+
+
+def test_step_topology_change_reinstantiates():
+    # an empty scan drops its endpoint launch: the graph is re-instantiated and
+    # the results still match the oracle
+    w = synth.workload(3)
+    f = w.frames[0]
+    m = GvomMap(w.grid, max_points_per_frame=f.n_points)
+    om = O.OracleMap(w.grid)
+    empty = dataclasses.replace(f.scans[1], points=f.scans[1].points[:0])
+    seq = [list(f.scans), [f.scans[0], empty, f.scans[2]], list(f.scans)]
+    for scans in seq:
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in scans])
+        m.step(f.vehicle_xyz, [to_dev(s) for s in scans], export=False)
+        compare_layers(layers_np(m), om.compute_maps())
+    st = m.graph_stats()
+    assert st["graph_launches"] == 3 and st["instantiations"] == 3, st
+
+
+def test_step_sensor_outside_rejected_before_capture():
+    w = synth.workload(1)
+    f = w.frames[0]
+    m = GvomMap(w.grid, max_points_per_frame=f.n_points)
+    m.step(f.vehicle_xyz, [to_dev(s) for s in f.scans])
+    before = layers_np(m)
+    far = synth.pose_matrix(np.eye(3), (500.0, 0.0, 0.0))
+    with pytest.raises(SensorOutside):
+        m.step(f.vehicle_xyz, [(torch.from_numpy(f.scans[0].points).cuda(), far, 64)])
+    m.compute_maps()
+    after = layers_np(m)
+    for k in before:
+        assert np.array_equal(np.nan_to_num(before[k], nan=-7), np.nan_to_num(after[k], nan=-7))
+    # the handle still works, through the graph
+    m.step(f.vehicle_xyz, [to_dev(s) for s in f.scans])
+    assert m.graph_stats()["graph_launches"] == 2
