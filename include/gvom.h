@@ -80,7 +80,11 @@ typedef struct gvom_config {
   int32_t slope_window;          /* N of the N x N plane fit, odd, 3..9          */
   int32_t min_plane_points;      /* >= 3 defined cells for a fit (reading A22)           */
   double neg_obs_threshold;      /* Delta-H in metres, flag iff larger    */
-  int32_t neg_obs_search_cells;  /* cone search distance in cells, >= 1          */
+  int32_t neg_obs_search_cells;  /* cone search distance K in cells, >= 1, with
+                                    (K + 3) * nz' * 65536 < 2^32 (nz' = nz rounded up to a
+                                    power of two: packed sweep keys) and
+                                    48 * max(nx, ny) + 64 * K < ~227 KiB (the sweep's
+                                    shared-memory ring); else GVOM_E_INVALID             */
   int32_t pad1;
 } gvom_config;
 

@@ -36,6 +36,12 @@ struct Layout {
   int64_t cap, nblk, cells;
 };
 
+int neg_qbits(int nz) {
+  int b = 0;
+  while ((1 << b) < nz) ++b;
+  return 16 + b;
+}
+
 bool valid_config(const gvom_config* c) {
   if (!c) return false;
   if (c->nx < 1 || c->ny < 1 || c->nz < 1 || c->nz > 2048) return false;
@@ -50,6 +56,10 @@ bool valid_config(const gvom_config* c) {
   if (c->slope_window < 3 || c->slope_window > 9 || (c->slope_window % 2) == 0) return false;
   if (c->min_plane_points < 3) return false;
   if (!(c->neg_obs_threshold >= 0) || c->neg_obs_search_cells < 1) return false;
+  // packed cone-sweep keys: (K + 3) << qb < 2^32 with qb = 16 + ceil(log2 nz)
+  if ((int64_t)(c->neg_obs_search_cells + 3) << neg_qbits(c->nz) >= (1ll << 32)) return false;
+  // the cone sweep's shared-memory ring holds at least two key lines
+  if (!neg_sweep_fits(c->nx > c->ny ? c->nx : c->ny, c->neg_obs_search_cells)) return false;
   if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES)) return false;
   return true;
 }
@@ -97,8 +107,8 @@ Layout make_layout(const gvom_config* c) {
   off += 3 * align_up((size_t)l.cells);
   l.qs = off;
   off += align_up(4 * (size_t)l.cells);
-  l.defbits = off;  // qsT, nmin, nmax for the negative-obstacle cone sweeps
-  l.defbits_bytes = 3 * align_up(4 * (size_t)l.cells);
+  l.defbits = off;  // nmin, nmax, negA, negB, negAT, negBT (cone sweeps)
+  l.defbits_bytes = 6 * align_up(4 * (size_t)l.cells);
   off += l.defbits_bytes;
   l.mbits = off;
   off += align_up(4 * (size_t)d.W);
@@ -358,9 +368,16 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->layers.soft = (uint8_t*)(h->ws + lay.layers_u8 + u8);
   h->layers.neg = (uint8_t*)(h->ws + lay.layers_u8 + 2 * u8);
   h->layers.qs = (int32_t*)(h->ws + lay.qs);
-  h->layers.qsT = (int32_t*)(h->ws + lay.defbits);
-  h->layers.nmin = (int32_t*)(h->ws + lay.defbits + align_up(4 * (size_t)lay.cells));
-  h->layers.nmax = (int32_t*)(h->ws + lay.defbits + 2 * align_up(4 * (size_t)lay.cells));
+  {
+    const size_t c4 = align_up(4 * (size_t)lay.cells);
+    char* b = h->ws + lay.defbits;
+    h->layers.nmin = (int32_t*)b;
+    h->layers.nmax = (int32_t*)(b + c4);
+    h->layers.negA = (uint32_t*)(b + 2 * c4);
+    h->layers.negB = (uint32_t*)(b + 3 * c4);
+    h->layers.negAT = (uint32_t*)(b + 4 * c4);
+    h->layers.negBT = (uint32_t*)(b + 5 * c4);
+  }
   h->mbits = (uint32_t*)(h->ws + lay.mbits);
   h->tc.tile = (uint32_t*)(h->ws + lay.tilecnt);
   h->tc.offset = h->tc.tile + n_tiles(h->d);
@@ -375,6 +392,7 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.slope_window = cfg->slope_window;
   h->lp.min_plane_points = cfg->min_plane_points;
   h->lp.neg_cells = cfg->neg_obs_search_cells;
+  h->lp.neg_qb = neg_qbits(cfg->nz);
   h->lp.skip_obstacles = (cfg->flags & GVOM_FLAG_SLOPE_SKIP_OBSTACLES) ? 1 : 0;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
@@ -970,7 +988,7 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
     return GVOM_OK;
   }
   GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
-                [&] { return launch_transpose_init(h->d, h->layers, h->st); }));
+                [&] { return launch_transpose_init(h->d, h->lp, h->layers, h->st); }));
   GVOM_CU(surface_layers(h));
   h->maps_valid = true;
   return GVOM_OK;

@@ -56,7 +56,12 @@ struct LayerPtrs {
   float* cost;    // costmap scratch (gvom_costmap, NEXT-4)
   float* spread;  // variance of the surface voxel's returns (NEXT-3)
   int32_t* qs;    // [ny][nx] fixed-point surface q_s, kQsUndef if undefined
-  int32_t* qsT;   // [nx][ny] transposed copy (cone sweeps along x read it by line)
+  // cone-sweep keys of the surface (see neg_keys): [ny][nx] and transposed
+  // [nx][ny] copies, so that every sweep reads its lines contiguously
+  uint32_t* negA;
+  uint32_t* negB;
+  uint32_t* negAT;
+  uint32_t* negBT;
   int32_t* nmin;  // [ny][nx] min / max of the heights found by the cone search
   int32_t* nmax;
 };
@@ -67,7 +72,42 @@ struct LayerParams {
   int64_t o_z;
   int32_t slope_window, min_plane_points, neg_cells;
   int32_t skip_obstacles;  // GVOM_FLAG_SLOPE_SKIP_OBSTACLES
+  int32_t neg_qb;          // q_s < 2^neg_qb (= 16 + ceil(log2 nz)); see neg_keys
 };
+
+// Cone-sweep keys (k_negative): a found ring (distance D, heights q) is packed
+// as (D << qb) | q for the minimum and (D << qb) | (2^qb - 1 - q) for the
+// maximum, so ONE unsigned min over sub-cones yields the least D and, among
+// the sub-cones attaining it, the least (resp. greatest) height -- exactly the
+// recurrence's tie rule.  An undefined cell is "not found" = (K + 1) << qb.
+// gvom_create guarantees (K + 3) << qb < 2^32 (no overflow when adding 1 << qb
+// to the not-found key).
+__host__ __device__ inline void neg_keys(int32_t q, const LayerParams& lp, uint32_t& ka,
+                                         uint32_t& kb) {
+  const uint32_t one = 1u << lp.neg_qb;
+  if (q == kQsUndef) {
+    ka = kb = (uint32_t)(lp.neg_cells + 1) << lp.neg_qb;
+  } else {
+    ka = one + (uint32_t)q;
+    kb = one + (one - 1u - (uint32_t)q);
+  }
+}
+
+// k_negative shared memory: a ring of R slots, each one key line of A keys and
+// one of B keys; the key of cross position bb sits at [neg_guard_left + bb],
+// with not-found guards over bb in [-K-1, -1] and [B, B+K] and the TMA
+// destination (bb = 0) 16-byte aligned; plus 4 state lines of B + 2K + 2.
+constexpr int kNegRing = 32;                                  // max ring slots
+constexpr size_t kNegSmemMax = 227 * 1024 - 2 * kNegRing * 8;  // minus mbarriers
+__host__ __device__ inline int neg_guard_left(int K) { return (K + 1 + 3) & ~3; }
+__host__ __device__ inline int neg_line_stride(int B, int K) {
+  return (neg_guard_left(K) + B + K + 1 + 3) & ~3;
+}
+inline size_t neg_slot_bytes(int B, int K) { return 8 * (size_t)neg_line_stride(B, K); }
+inline size_t neg_state_bytes(int B, int K) { return 16 * ((size_t)B + 2 * (size_t)K + 2); }
+inline bool neg_sweep_fits(int B, int K) {
+  return neg_state_bytes(B, K) + 2 * neg_slot_bytes(B, K) <= kNegSmemMax;
+}
 
 // ---- launchers (each launches exactly one kernel; returns cudaError_t) ----
 // Occupancy counts per finalize tile, kept by the ray cast as bits are set;
@@ -139,7 +179,8 @@ cudaError_t launch_tile_scan(const TileCounts& tc, int64_t t_begin, int64_t t_en
                              cudaStream_t st);
 cudaError_t launch_endpoint_records(const EpRecord* ep, int64_t n, const int32_t* lut,
                                     gvom_voxel* data, cudaStream_t st);
-cudaError_t launch_transpose_init(const Dims& d, const LayerPtrs& out, cudaStream_t st);
+cudaError_t launch_transpose_init(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                                  cudaStream_t st);
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st);
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,

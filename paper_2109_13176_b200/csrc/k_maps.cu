@@ -203,7 +203,14 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   out.nmax[c] = INT32_MIN;
   const int32_t qv = zs < 0 ? kQsUndef : (int32_t)q_s;
   out.qs[c] = qv;
-  out.qsT[(int64_t)x * d.ny + y] = qv;
+  {
+    uint32_t ka, kb;
+    neg_keys(qv, lp, ka, kb);
+    out.negA[c] = ka;
+    out.negB[c] = kb;
+    out.negAT[(int64_t)x * d.ny + y] = ka;
+    out.negBT[(int64_t)x * d.ny + y] = kb;
+  }
   if (zs < 0) {
     out.height[c] = __int_as_float(0x7fc00000);
     out.density[c] = __int_as_float(0x7fc00000);
@@ -322,16 +329,19 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
 //   D(x,y) = 1                       if ring 1 (x+1, y-1..y+1) has a defined cell
 //          = 1 + min_t D(x+1, y+t)   otherwise (capped: > K = not found),
 // and Mn / Mx are the min / max over the sub-cones attaining that minimum
-// (their first rings are exactly the pieces of ring D of (x,y)).  The other
-// cones are the same sweep mirrored / transposed.  Apexes outside the map in
-// the cross direction (up to K cells) take part, since their cones reach in.
-// A block sweeps a tile of T lines plus a K-line halo (D <= K depends on at
-// most K lines ahead); every found (Mn, Mx) is folded into the cell's
-// nmin / nmax with atomics, and k_slope applies "max - min > T_neg".
-// Lines are streamed into a shared-memory ring by 1D TMA bulk copies
-// (cp.async.bulk, mbarrier completion) kNegRing lines ahead of the sweep.
-constexpr int kNegRing = 32;
-
+// (their first rings are exactly the pieces of ring D of (x,y)).  With the
+// packed keys of neg_keys this is, per key, ONE branch-free min:
+//   key(x,y) = min( min_t key_ring1(x+1, y+t),  min_t key(x+1, y+t) + (1 << qb),
+//                   not-found ).
+// The other cones are the same sweep mirrored / transposed.  Apexes outside
+// the map in the cross direction (up to K cells) take part, since their cones
+// reach in.  A block sweeps a tile of T lines plus a K-line halo (D <= K
+// depends on at most K lines ahead); every found (Mn, Mx) is folded into the
+// cell's nmin / nmax with atomics, and k_neg_decide applies
+// "max - min > T_neg".  Key lines are streamed into a shared-memory ring by
+// 1D TMA bulk copies (cp.async.bulk, mbarrier completion) up to kNegRing lines
+// ahead of the sweep; each ring line carries not-found guard cells on both
+// sides, so no apex position needs a bounds check.
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
                    (uint32_t)__cvta_generic_to_shared(bar)),
@@ -346,14 +356,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// one elected thread: expect `bytes` on `bar`, then bulk-copy global -> shared
-__device__ __forceinline__ void tma_line(void* dst, const void* src, uint32_t bytes,
+// bulk-copy global -> shared, completing `bytes` of the transaction count on
+// `bar` (the caller announced them with mbarrier.arrive.expect_tx)
+__device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
   const uint32_t dsm = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-               : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
           "r"(dsm),
@@ -362,7 +371,7 @@ __device__ __forceinline__ void tma_line(void* dst, const void* src, uint32_t by
 }
 
 // a ring slot whose line lies outside the map completes its phase empty, so
-// every slot's phase parity stays (step / kNegRing) & 1
+// every slot's phase parity stays (step / R) & 1
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
                    (uint32_t)__cvta_generic_to_shared(bar))
@@ -370,12 +379,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // Warp-specialised: the last warp is the producer (TMA bulk copies of the
-// ring-1 lines, kNegRing slots ahead, guarded by full/empty mbarriers); the
-// other warps are consumers (one apex position each per pass) and sync among
+// ring-1 key lines, R slots ahead, guarded by full/empty mbarriers); the other
+// warps are consumers (apex positions strided over them) and sync among
 // themselves with a named barrier once per line.
 __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerParams lp,
-                                                        const LayerPtrs out, int T) {
-  extern __shared__ __align__(16) int32_t sm[];
+                                                        const LayerPtrs out, int T, int R) {
+  extern __shared__ __align__(16) uint32_t sm[];
   __shared__ __align__(8) uint64_t full[kNegRing], empty[kNegRing];
   const int cone = blockIdx.y;               // 0:+x 1:-x 2:+y 3:-y
   const bool alongx = cone < 2;              // sweep over x (lines = columns)
@@ -384,17 +393,19 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   const int B = alongx ? d.ny : d.nx;        // cross positions per line
   const int K = lp.neg_cells;
   const int NB = B + 2 * K + 2;              // apex cross positions -K-1 .. B+K
-  const int BP = (B + 3) & ~3;               // ring line stride (16-byte rows)
+  const int GL = neg_guard_left(K);
+  const int LS = neg_line_stride(B, K);      // one key line (A or B keys)
   const int nthr = blockDim.x - 32;          // consumer threads
-  int32_t* ring = sm;                        // [kNegRing][BP]
-  int32_t* Dp = ring + kNegRing * BP;        // state of the previous line
-  int32_t* Dn = Dp + NB;
-  int32_t* Mnp = Dn + NB;
-  int32_t* Mnn = Mnp + NB;
-  int32_t* Mxp = Mnn + NB;
-  int32_t* Mxn = Mxp + NB;
-  const int32_t* __restrict__ src = alongx ? out.qsT : out.qs;  // line-contiguous
-  const int INF = K + 1;
+  const uint32_t ONE = 1u << lp.neg_qb;
+  const uint32_t NF = (uint32_t)(K + 1) << lp.neg_qb;  // not found
+  const uint32_t QM = ONE - 1u;
+  uint32_t* ring = sm;                       // [R][2][LS]
+  uint32_t* Ap = ring + (size_t)R * 2 * LS;  // sweep state (previous / next line)
+  uint32_t* An = Ap + NB;
+  uint32_t* Bp = An + NB;
+  uint32_t* Bn = Bp + NB;
+  const uint32_t* __restrict__ srcA = alongx ? out.negAT : out.negA;  // line-contiguous
+  const uint32_t* __restrict__ srcB = alongx ? out.negBT : out.negB;
   const int p0 = blockIdx.x * T;             // tile lines [p0, p0+T)
   if (p0 >= A) return;                       // grid sized for max(nx, ny)
   const int p1 = min(A, p0 + T);
@@ -410,12 +421,16 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   const uint32_t line_bytes = (uint32_t)B * 4u;
   auto line_of = [&](int st) { return pstart - dir * st + dir; };  // ring-1 line of step st
   for (int i = threadIdx.x; i < NB; i += blockDim.x) {
-    Dp[i] = Dn[i] = INF;  // both buffers: guard cells are never rewritten
-    Mnp[i] = Mnn[i] = INT32_MAX;
-    Mxp[i] = Mxn[i] = INT32_MIN;
+    Ap[i] = An[i] = NF;  // both buffers: guard apexes are never rewritten
+    Bp[i] = Bn[i] = NF;
+  }
+  // guard cells of every ring line (the TMA writes only [GL, GL + B))
+  for (int i = threadIdx.x; i < R * 2 * (LS - B); i += blockDim.x) {
+    const int line = i / (LS - B), g = i - line * (LS - B);
+    ring[(size_t)line * LS + (g < GL ? g : g + B)] = NF;
   }
   if (threadIdx.x == 0) {
-    for (int j = 0; j < kNegRing; ++j) {
+    for (int j = 0; j < R; ++j) {
       mbar_init(&full[j], 1);
       mbar_init(&empty[j], 1);
     }
@@ -425,71 +440,77 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   if (threadIdx.x >= nthr) {
     // ---------------- producer warp ----------------
     if (threadIdx.x == nthr) {
+      int j = 0;
+      uint32_t ph = 0;  // phase parity of the current pass over the ring
       for (int st = 0; st < nsteps; ++st) {
-        const int j = st % kNegRing;
-        if (st >= kNegRing) mbar_wait(&empty[j], (uint32_t)(((st / kNegRing) - 1) & 1));
+        if (st >= R) mbar_wait(&empty[j], ph ^ 1u);
         const int pl = line_of(st);
-        if (tma && pl >= 0 && pl < A)
-          tma_line(ring + j * BP, src + (int64_t)pl * B, line_bytes, &full[j]);
-        else
+        if (tma && pl >= 0 && pl < A) {
+          uint32_t* dst = ring + (size_t)j * 2 * LS + GL;
+          const uint32_t b = (uint32_t)__cvta_generic_to_shared(&full[j]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                       "r"(2u * line_bytes)
+                       : "memory");
+          tma_copy(dst, srcA + (int64_t)pl * B, line_bytes, &full[j]);
+          tma_copy(dst + LS, srcB + (int64_t)pl * B, line_bytes, &full[j]);
+        } else {
           mbar_arrive(&full[j]);
+        }
+        if (++j == R) {
+          j = 0;
+          ph ^= 1u;
+        }
       }
     }
     return;
   }
   // ---------------- consumers ----------------
+  int j = 0;
+  uint32_t ph = 0;  // phase parity of the current pass over the ring
   for (int st = 0; st < nsteps; ++st) {
     const int p = pstart - dir * st;
     const int pl = p + dir;
     const bool inmap = pl >= 0 && pl < A;
-    const int j = st % kNegRing;
-    int32_t* lq = ring + j * BP;
-    mbar_wait(&full[j], (uint32_t)((st / kNegRing) & 1));
+    const bool emit = p >= p0 && p < p1;
+    uint32_t* la = ring + (size_t)j * 2 * LS;
+    uint32_t* lb = la + LS;
+    mbar_wait(&full[j], ph);
     if (inmap && !tma) {  // rows not 16-byte multiples: plain loads
-      for (int b = threadIdx.x; b < B; b += nthr) lq[b] = __ldg(src + (int64_t)pl * B + b);
-      asm volatile("bar.sync 1, %0;" ::"r"(nthr));
+      for (int b = threadIdx.x; b < B; b += nthr) {
+        la[GL + b] = __ldg(srcA + (int64_t)pl * B + b);
+        lb[GL + b] = __ldg(srcB + (int64_t)pl * B + b);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     }
+    // apex i (cross b = i - K - 1): ring-1 taps b-1..b+1 at la[GL + b - 1 ..]
+    const uint32_t* ta = la + GL - K - 2;
+    const uint32_t* tb = lb + GL - K - 2;
     for (int i = threadIdx.x + 1; i < NB - 1; i += nthr) {
-      const int b = i - K - 1;  // apex cross position
-      int Dv = INF, mn = INT32_MAX, mx = INT32_MIN;
-      if (inmap) {  // ring 1: cross b-1..b+1 of line pl (in-map only)
-#pragma unroll
-        for (int t = -1; t <= 1; ++t) {
-          const int bb = b + t;
-          if (bb >= 0 && bb < B) {
-            const int32_t q = lq[bb];
-            if (q != kQsUndef) {
-              Dv = 1;
-              mn = min(mn, q);
-              mx = max(mx, q);
-            }
-          }
-        }
+      uint32_t ka = min(min(Ap[i - 1], Ap[i]), Ap[i + 1]) + ONE;
+      uint32_t kb = min(min(Bp[i - 1], Bp[i]), Bp[i + 1]) + ONE;
+      if (inmap) {
+        ka = min(ka, min(min(ta[i], ta[i + 1]), ta[i + 2]));
+        kb = min(kb, min(min(tb[i], tb[i + 1]), tb[i + 2]));
       }
-      if (Dv != 1) {
-        const int d0 = Dp[i - 1], d1 = Dp[i], d2 = Dp[i + 1];
-        const int dm = min(d0, min(d1, d2));
-        if (dm < K) {
-          Dv = dm + 1;
-          if (d0 == dm) { mn = min(mn, Mnp[i - 1]); mx = max(mx, Mxp[i - 1]); }
-          if (d1 == dm) { mn = min(mn, Mnp[i]); mx = max(mx, Mxp[i]); }
-          if (d2 == dm) { mn = min(mn, Mnp[i + 1]); mx = max(mx, Mxp[i + 1]); }
-        }
-      }
-      Dn[i] = Dv;
-      Mnn[i] = mn;
-      Mxn[i] = mx;
-      if (Dv <= K && b >= 0 && b < B && p >= p0 && p < p1) {
+      ka = min(ka, NF);
+      kb = min(kb, NF);
+      An[i] = ka;
+      Bn[i] = kb;
+      const int b = i - K - 1;
+      if (emit && ka < NF && (unsigned)b < (unsigned)B) {
         const int64_t cell = alongx ? (int64_t)b * d.nx + p : (int64_t)p * d.nx + b;
-        atomicMin(out.nmin + cell, mn);
-        atomicMax(out.nmax + cell, mx);
+        atomicMin(out.nmin + cell, (int32_t)(ka & QM));
+        atomicMax(out.nmax + cell, (int32_t)(QM - (kb & QM)));
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");  // state + slot j consumed
     if (threadIdx.x == 0) mbar_arrive(&empty[j]);
-    int32_t* t0 = Dp; Dp = Dn; Dn = t0;
-    t0 = Mnp; Mnp = Mnn; Mnn = t0;
-    t0 = Mxp; Mxp = Mxn; Mxn = t0;
+    if (++j == R) {
+      j = 0;
+      ph ^= 1u;
+    }
+    uint32_t* t0 = Ap; Ap = An; An = t0;
+    t0 = Bp; Bp = Bn; Bn = t0;
   }
 }
 
@@ -644,22 +665,31 @@ cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& 
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                             cudaStream_t st) {
   const int A = d.nx > d.ny ? d.nx : d.ny, B = A;
+  const int K = lp.neg_cells;
   // tiles: about one block per SM over the 4 cones, at least 8 lines each
   int T = (4 * A + 147) / 148;
   T = T < 8 ? 8 : ((T + 7) / 8) * 8;
-  const size_t NB = (size_t)B + 2 * (size_t)lp.neg_cells + 2;
-  const size_t BP = ((size_t)B + 3) & ~(size_t)3;
-  const size_t smem = sizeof(int32_t) * (6 * NB + kNegRing * BP);
+#ifdef GVOM_NEG_T
+  T = GVOM_NEG_T;
+#endif
+  const size_t NB = (size_t)B + 2 * (size_t)K + 2;
+  const size_t slot = neg_slot_bytes(B, K), state = neg_state_bytes(B, K);
+  // ring depth: as many slots as shared memory allows, up to kNegRing
+  // (gvom_create guarantees at least 2, neg_sweep_fits)
+  if (!neg_sweep_fits(B, K)) return cudaErrorInvalidConfiguration;
+  int R = (int)((kNegSmemMax - state) / slot);
+  R = R > kNegRing ? kNegRing : R;
+  const size_t smem = state + (size_t)R * slot;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(
         k_negative, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  // consumers: one apex position each per pass (up to 1024), + 1 producer warp
+  // consumers: one apex position each per pass (up to 992), + 1 producer warp
   int nthr = (int)((NB - 2 + 31) / 32) * 32;
-  if (nthr > 1024 - 32) nthr = 1024 - 32;  // + the producer warp <= 1024 threads
+  if (nthr > 1024 - 32) nthr = 1024 - 32;
   const dim3 grid((unsigned)((A + T - 1) / T), 4);
-  k_negative<<<grid, nthr + 32, smem, st>>>(d, lp, out, T);
+  k_negative<<<grid, nthr + 32, smem, st>>>(d, lp, out, T, R);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_neg_decide<<<cells_blocks(d, 256), 256, 0, st>>>(d, lp, out);

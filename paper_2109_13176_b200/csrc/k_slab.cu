@@ -160,12 +160,19 @@ __global__ void __launch_bounds__(256) k_endpoint_records(const EpRecord* __rest
             (unsigned long long)r.dz * (unsigned long long)r.dz);
 }
 
-// after the surface all-gather: transposed copy + cone-search accumulators
-__global__ void __launch_bounds__(256) k_transpose_init(const Dims d, const LayerPtrs out) {
+// after the surface all-gather: cone-sweep keys (+ transposed copies) and the
+// cone-search accumulators
+__global__ void __launch_bounds__(256) k_transpose_init(const Dims d, const LayerParams lp,
+                                                        const LayerPtrs out) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= (int64_t)d.nx * d.ny) return;
   const int x = (int)(c % d.nx), y = (int)(c / d.nx);
-  out.qsT[(int64_t)x * d.ny + y] = out.qs[c];
+  uint32_t ka, kb;
+  neg_keys(out.qs[c], lp, ka, kb);
+  out.negA[c] = ka;
+  out.negB[c] = kb;
+  out.negAT[(int64_t)x * d.ny + y] = ka;
+  out.negBT[(int64_t)x * d.ny + y] = kb;
   out.nmin[c] = INT32_MAX;
   out.nmax[c] = INT32_MIN;
 }
@@ -209,8 +216,9 @@ cudaError_t launch_endpoint_records(const EpRecord* ep, int64_t n, const int32_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_transpose_init(const Dims& d, const LayerPtrs& out, cudaStream_t st) {
-  k_transpose_init<<<blocks_for((int64_t)d.nx * d.ny, 256), 256, 0, st>>>(d, out);
+cudaError_t launch_transpose_init(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                                  cudaStream_t st) {
+  k_transpose_init<<<blocks_for((int64_t)d.nx * d.ny, 256), 256, 0, st>>>(d, lp, out);
   return cudaGetLastError();
 }
 
