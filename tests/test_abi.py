@@ -61,6 +61,25 @@ def test_workspace_sizing(lib):
     assert gvom.workspace_bytes(bad, 10) == 0
 
 
+def test_cone_search_limits(lib):
+    # packed sweep keys: (K + 3) << (16 + ceil(log2 nz)) < 2^32 (include/gvom.h)
+    g = synth.grid_cfg(64, 64, 2048, 0.25)
+    for K, ok in ((28, True), (29, False), (60, False)):
+        g["neg_obs_search_cells"] = K
+        assert (gvom.workspace_bytes(g, 10) > 0) == ok, K
+    g = synth.grid_cfg(64, 64, 1000, 0.25)  # nz rounds up to 1024
+    for K, ok in ((60, True), (61, False)):
+        g["neg_obs_search_cells"] = K
+        assert (gvom.workspace_bytes(g, 10) > 0) == ok, K
+    # the sweep's shared-memory ring must hold two key lines of max(nx, ny)
+    g = synth.grid_cfg(4096, 8, 8, 0.25)
+    g["neg_obs_search_cells"] = 8
+    assert gvom.workspace_bytes(g, 10) > 0
+    g = synth.grid_cfg(8192, 8, 8, 0.25)
+    g["neg_obs_search_cells"] = 8
+    assert gvom.workspace_bytes(g, 10) == 0
+
+
 def test_create_rejects_bad_arguments(lib):
     cfg = gvom.make_config(synth.grid_cfg(8, 8, 8, 0.25), 16)
     h = C.c_void_p()
