@@ -89,6 +89,18 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_traffic(workload: str):
+    """DRAM bytes per k_raycast launch (read + write) for this workload from the
+    committed ncu --set full capture (profiles/raycast_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "raycast_traffic.json")
+    try:
+        d = json.load(open(p))
+        v = d["bytes_per_launch"].get(workload)
+        return (float(v), d["source"][workload]) if v is not None else (None, None)
+    except Exception:
+        return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -428,6 +440,7 @@ def main():
     e2e_value = npts * e2e_steps * world / (e2e_ms / 1e3)
 
     peak, peak_src = peaks()
+    traffic, traffic_src = measured_traffic(w.name)
     ray_ms, ray_n = stage["raycast"]
     ray_launch_ms = ray_ms / max(ray_n, 1)
     scans_per_frame = len(frames[0].scans)
@@ -458,8 +471,9 @@ def main():
             "graph": gstats,
             "map_updates_per_s": world * args.steps / (total_ms / 1e3),
             "roofline": {"bound": "hbm", "kernel": "k_raycast", "achieved": ray_gbs,
-                         "peak": peak, "unit": "GB/s", "frac": ray_gbs / peak, "traffic": None,
-                         "peak_source": peak_src, "launch_ms": ray_launch_ms,
+                         "peak": peak, "unit": "GB/s", "frac": ray_gbs / peak, "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
+                         "launch_ms": ray_launch_ms,
                          "bytes_per_launch": ray_bytes,
                          "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)"},
             "integrate": {"ms_per_frame": integ_ms, "points_per_s": npts / (integ_ms / 1e3),
