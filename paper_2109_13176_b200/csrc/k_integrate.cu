@@ -250,12 +250,11 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
   k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
 }
 
+// The rays of one warp (32 consecutive thread ids gtid of the batch).
 template <bool kStream>
-__global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatch rb,
-                                                 const Dims d, uint32_t* __restrict__ miss,
-                                                 uint32_t* __restrict__ bits,
-                                                 const TileCounts tc, bool last_sensor) {
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
+                                         uint32_t* __restrict__ miss, uint32_t* __restrict__ bits,
+                                         const TileCounts& tc, int64_t gtid) {
   const int64_t gt = gtid / rb.tile_threads;  // interleaved (tile, sensor)
   const int sidx = (int)(gt % rb.S);
   const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
@@ -407,6 +406,14 @@ __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatc
       dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
     }
   }
+}
+
+template <bool kStream>
+__global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RayBatch rb,
+                                                 const Dims d, uint32_t* __restrict__ miss,
+                                                 uint32_t* __restrict__ bits,
+                                                 const TileCounts tc, bool last_sensor) {
+  ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
 
@@ -864,7 +871,8 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   // schedule by where the REDs land (see aggregate_red_*): the resident one
   // also needs byte offsets < 2^32
   const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
-  if (miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32))
+  const bool stream = !(miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32));
+  if (!stream)
     k_raycast<false><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   else
     k_raycast<true><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
