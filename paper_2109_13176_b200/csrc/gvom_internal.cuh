@@ -141,20 +141,12 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
                                   cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1);
-cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
-                              cudaStream_t st);
-cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
-                             cudaStream_t st);
-cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const uint32_t* wprefix,
-                            gvom_voxel* data, const Dims& d, cudaStream_t st);
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st);
 // zeroes a[0:abytes), b[0:bbytes), c[0:cbytes) (multiples of 16, 16-byte aligned)
 cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
                          cudaStream_t st);
-cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
-                               const Dims& d, cudaStream_t st);
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
                             const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st);
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,

@@ -430,157 +430,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
   return v;
 }
 
-// popcount of a block's 1024 bitmask words
-__global__ void __launch_bounds__(kRankThreads) k_rank_count(const uint32_t* __restrict__ bits,
-                                                             int64_t W,
-                                                             uint32_t* __restrict__ block_sums) {
-  __shared__ uint32_t wsum[kRankThreads / 32];
-  const int64_t base = (int64_t)blockIdx.x * kRankWordsPerBlock + threadIdx.x * 4;
-  uint32_t c = 0;
-  if (base + 3 < W) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(bits + base));
-    c = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-  } else {
-    for (int i = 0; i < 4; ++i)
-      if (base + i < W) c += __popc(bits[base + i]);
-  }
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int i = 0; i < kRankThreads / 32; ++i) t += wsum[i];
-    block_sums[blockIdx.x] = t;
-  }
-}
-
-// exclusive scan of the block sums (one CTA); total -> *total
-__global__ void __launch_bounds__(1024) k_rank_scan(uint32_t* __restrict__ sums, int64_t nblk,
-                                                    uint32_t* __restrict__ total) {
-  __shared__ uint32_t wsum[32];
-  __shared__ uint32_t carry;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nblk; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const uint32_t v = i < nblk ? sums[i] : 0u;
-    const uint32_t inc = warp_incl_scan(v, lane);
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const uint32_t w = wsum[lane];
-      wsum[lane] = warp_incl_scan(w, lane) - w;
-    }
-    __syncthreads();
-    const uint32_t excl = carry + wsum[wid] + inc - v;
-    if (i < nblk) sums[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-}
-
-// Block-local per-word prefix of the tile's 1024 words into smem; returns
-// nothing, fills spre[] (absolute word prefix) and sbits[].
-__device__ __forceinline__ void tile_prefix(const uint32_t* __restrict__ bits, int64_t W,
-                                            uint32_t boff, uint32_t* sbits, uint32_t* spre,
-                                            uint32_t* wsum) {
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int64_t base = (int64_t)blockIdx.x * kRankWordsPerBlock + t * 4;
-  uint32_t w4[4];
-  if (base + 3 < W) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(bits + base));
-    w4[0] = v.x;
-    w4[1] = v.y;
-    w4[2] = v.z;
-    w4[3] = v.w;
-  } else {
-    for (int i = 0; i < 4; ++i) w4[i] = (base + i < W) ? bits[base + i] : 0u;
-  }
-  const uint32_t c0 = __popc(w4[0]), c1 = __popc(w4[1]), c2 = __popc(w4[2]), c3 = __popc(w4[3]);
-  const uint32_t tsum = c0 + c1 + c2 + c3;
-  const uint32_t inc = warp_incl_scan(tsum, lane);
-  if (lane == 31) wsum[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    const uint32_t w = lane < kRankThreads / 32 ? wsum[lane] : 0u;
-    const uint32_t e = warp_incl_scan(w, lane) - w;
-    if (lane < kRankThreads / 32) wsum[lane] = e;
-  }
-  __syncthreads();
-  const uint32_t p0 = boff + wsum[wid] + inc - tsum;
-  sbits[4 * t + 0] = w4[0];
-  sbits[4 * t + 1] = w4[1];
-  sbits[4 * t + 2] = w4[2];
-  sbits[4 * t + 3] = w4[3];
-  spre[4 * t + 0] = p0;
-  spre[4 * t + 1] = p0 + c0;
-  spre[4 * t + 2] = p0 + c0 + c1;
-  spre[4 * t + 3] = p0 + c0 + c1 + c2;
-  __syncthreads();
-}
-
-__device__ __forceinline__ void store_prefix(uint32_t* __restrict__ wprefix, int64_t W,
-                                             const uint32_t* spre) {
-  const int t = threadIdx.x;
-  const int64_t base = (int64_t)blockIdx.x * kRankWordsPerBlock + t * 4;
-  if (base + 3 < W) {
-    *reinterpret_cast<uint4*>(wprefix + base) =
-        make_uint4(spre[4 * t], spre[4 * t + 1], spre[4 * t + 2], spre[4 * t + 3]);
-  } else {
-    for (int i = 0; i < 4; ++i)
-      if (base + i < W) wprefix[base + i] = spre[4 * t + i];
-  }
-}
-
-// O6 in place: buf[L] holds the miss count; becomes rank (occupied) or
-// -1 - min(N_m, 2^30) (empty).  Occupied rows get {0, misses, 0xFFFFFFFF, 0, 0, 0}
-// for the endpoint pass to accumulate into.  One thread per 4 voxels (one
-// 16-byte load + store); rank from the absolute per-word prefix.
-__global__ void __launch_bounds__(256) k_finalize(int32_t* __restrict__ buf,
-                                                  const uint32_t* __restrict__ bits,
-                                                  const uint32_t* __restrict__ wprefix,
-                                                  gvom_voxel* __restrict__ data, const Dims d) {
-  const int64_t L = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (L >= d.V) return;
-  const uint32_t bw = __ldg(bits + (L >> 5));
-  const uint32_t pre = __ldg(wprefix + (L >> 5));
-  const bool vec = (L + 3 < d.V);
-  uint32_t m[4];
-  if (vec) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(buf + L));
-    m[0] = v.x;
-    m[1] = v.y;
-    m[2] = v.z;
-    m[3] = v.w;
-  } else {
-    for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
-  }
-  int32_t o[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int bit = (int)((L + j) & 31);
-    if ((bw >> bit) & 1u) {
-      const uint32_t rank = pre + __popc(bw & ((1u << bit) - 1u));
-      o[j] = (int32_t)rank;
-      uint4* row = reinterpret_cast<uint4*>(data + rank);
-      row[0] = make_uint4(0u, m[j], 0xffffffffu, 0u);
-      row[1] = make_uint4(0u, 0u, 0u, 0u);
-    } else {
-      const uint32_t nm = m[j] < kMissSat ? m[j] : kMissSat;
-      o[j] = -1 - (int32_t)nm;
-    }
-  }
-  if (vec) {
-    *reinterpret_cast<int4*>(buf + L) = make_int4(o[0], o[1], o[2], o[3]);
-  } else {
-    for (int j = 0; j < 4; ++j)
-      if (L + j < d.V) buf[L + j] = o[j];
-  }
-}
-
 // Single-pass rank of the occupied voxels (decoupled look-back scan over the
 // occupancy bitmask): absolute exclusive popcount prefix per 32-voxel word, so
 // rank(L) = wprefix[L>>5] + popc(bits[L>>5] & ((1<<(L&31))-1)) is the voxel's
@@ -693,12 +542,14 @@ __global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na
   }
 }
 
-// Rank + O6 encode in one launch.  Block b owns tile b (256 bitmask words =
-// 8192 voxels): its rank offset is the sum of the super-tile counts before
-// its super-tile plus the tile counts before it inside it (both kept by the
-// ray cast), so no block waits on another.  Then: per-word prefix (block
-// scan), wprefix store, and the in-place LUT encode / data-row init of its
-// 8192 voxels with 16-byte accesses.
+// Rank + O6 encode in one launch (O6: buf[L] holds the miss count and
+// becomes the rank if occupied, else -1 - min(N_m, 2^30); occupied rows get
+// {0, misses, 0xFFFFFFFF, 0, 0, 0} for the endpoint pass).  Block b owns tile
+// b (256 bitmask words = 8192 voxels): its rank offset is the exclusive
+// prefix of the tile counts kept by the ray cast and scanned by its last
+// block, so no block waits on another.  Then: per-word prefix (block scan),
+// wprefix store, and the in-place LUT encode / data-row init of its 8192
+// voxels with 16-byte accesses.
 __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
     gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t_begin) {
@@ -777,18 +628,6 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
       }
     }
   }
-}
-
-// per-word absolute prefix only (merged-map export)
-__global__ void __launch_bounds__(kRankThreads) k_prefix_only(const uint32_t* __restrict__ bits,
-                                                              uint32_t* __restrict__ wprefix,
-                                                              const uint32_t* __restrict__ boff,
-                                                              const Dims d) {
-  __shared__ uint32_t sbits[kRankWordsPerBlock];
-  __shared__ uint32_t spre[kRankWordsPerBlock];
-  __shared__ uint32_t wsum[32];
-  tile_prefix(bits, d.W, boff[blockIdx.x], sbits, spre, wsum);
-  store_prefix(wprefix, d.W, spre);
 }
 
 // O4 per return: hits, min_dz, m1 = sum dz, m2 = sum dz^2 into the data row.
@@ -883,26 +722,6 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   return cudaGetLastError();
 }
 
-cudaError_t launch_rank_count(const uint32_t* bits, const Dims& d, uint32_t* block_sums,
-                              cudaStream_t st) {
-  k_rank_count<<<(unsigned)rank_blocks(d), kRankThreads, 0, st>>>(bits, d.W, block_sums);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_rank_scan(uint32_t* block_sums, int64_t nblk, uint32_t* total,
-                             cudaStream_t st) {
-  k_rank_scan<<<1, 1024, 0, st>>>(block_sums, nblk, total);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finalize(int32_t* lut_inplace, const uint32_t* bits, const uint32_t* wprefix,
-                            gvom_voxel* data, const Dims& d, cudaStream_t st) {
-  const int64_t threads = (d.V + 3) / 4;
-  k_finalize<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(lut_inplace, bits, wprefix, data,
-                                                                d);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st) {
@@ -931,12 +750,6 @@ cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, ui
   if (t_end <= t_begin) return cudaSuccess;
   k_finalize_tiles<<<(unsigned)(t_end - t_begin), kTileWords, 0, st>>>(lut_inplace, bits, wprefix,
                                                                        data, tc, d, t_begin);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_prefix_only(const uint32_t* bits, uint32_t* wprefix, const uint32_t* block_off,
-                               const Dims& d, cudaStream_t st) {
-  k_prefix_only<<<(unsigned)rank_blocks(d), kRankThreads, 0, st>>>(bits, wprefix, block_off, d);
   return cudaGetLastError();
 }
 
