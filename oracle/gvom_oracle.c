@@ -507,6 +507,79 @@ void or_negative(int32_t nx, int32_t ny, int32_t K, int64_t T_neg, const int32_t
 }
 
 /* ------------------------------------------------------------------------ */
+/* O10 variant: 8 cones ("D = 8 directions   */
+/* at half-angle 22.5 deg ... ring expansion in Chebyshev rings"; reading   */
+/* B8).  Cone j points at j*45 degrees.  An offset (u, v) is in cone j iff, */
+/* after rotating it by -90*(j/2) degrees ((u,v) -> (v,-u), j/2 times):     */
+/*   j even: U > 0 and |V| < (sqrt2 - 1) U   <=> (|V| + U)^2 < 2 U^2        */
+/*   j odd : U > 0, V > 0, (sqrt2 - 1) U < V < (sqrt2 + 1) U                */
+/*           <=> (U + V)^2 > 2 U^2 and (U + V)^2 > 2 V^2                    */
+/* tan(22.5) is irrational, so no nonzero integer offset lies on a cone     */
+/* boundary and the 8 cones partition the plane minus the origin.  The rest */
+/* is O10 unchanged: per cone, the first Chebyshev ring k = 1..K holding a  */
+/* defined in-map cell contributes all its defined cells of the cone to F.  */
+/* ------------------------------------------------------------------------ */
+int or_in_cone8(int64_t u, int64_t v, int j) {
+  for (int r = 0; r < j / 2; ++r) {
+    int64_t t = u;
+    u = v;
+    v = -t;
+  }
+  if (u <= 0) return 0;
+  if ((j & 1) == 0) {
+    int64_t a = (v < 0 ? -v : v) + u;
+    return a * a < 2 * u * u;
+  }
+  if (v <= 0) return 0;
+  int64_t s = u + v;
+  return s * s > 2 * u * u && s * s > 2 * v * v;
+}
+
+/* the cone holding offset (u, v), -1 if none or several (test hook)        */
+int or_cone8_of(int64_t u, int64_t v) {
+  int hit = -1, n = 0;
+  for (int j = 0; j < 8; ++j)
+    if (or_in_cone8(u, v, j)) {
+      hit = j;
+      n++;
+    }
+  return n == 1 ? hit : -1;
+}
+
+void or_negative8(int32_t nx, int32_t ny, int32_t K, int64_t T_neg, const int32_t* qs,
+                  const uint8_t* defined, uint8_t* neg) {
+  for (int64_t y = 0; y < ny; ++y)
+    for (int64_t x = 0; x < nx; ++x) {
+      int64_t c = x + (int64_t)nx * y;
+      neg[c] = 0;
+      if (defined[c]) continue;
+      int64_t fmin = INT64_MAX, fmax = INT64_MIN, fcount = 0;
+      for (int cone = 0; cone < 8; ++cone) {
+        for (int32_t k = 1; k <= K; ++k) {
+          int found = 0;
+          /* every cell at Chebyshev distance k */
+          for (int64_t v = -k; v <= k; ++v)
+            for (int64_t u = -k; u <= k; ++u) {
+              if ((u < 0 ? -u : u) != k && (v < 0 ? -v : v) != k) continue;
+              if (!or_in_cone8(u, v, cone)) continue;
+              int64_t xx = x + u, yy = y + v;
+              if (xx < 0 || xx >= nx || yy < 0 || yy >= ny) continue;
+              int64_t cc = xx + (int64_t)nx * yy;
+              if (!defined[cc]) continue;
+              found = 1;
+              int64_t q = qs[cc];
+              if (q < fmin) fmin = q;
+              if (q > fmax) fmax = q;
+              fcount++;
+            }
+          if (found) break;
+        }
+      }
+      neg[c] = (fcount >= 2 && (fmax - fmin) > T_neg) ? 1 : 0;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Costmap ("each of the output maps get some     */
 /* weight assigned to them and the resulting per pixel sum is the cost in   */
 /* that pixel").  Reading B5: a layer that is NaN (undefined) contributes 0; */

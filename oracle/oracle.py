@@ -70,6 +70,9 @@ def lib():
         _lib.or_slope_roughness.argtypes = [i32, i32, f64, i32, i32, P, P, P, P, P]
         _lib.or_spread.argtypes = [i32, i32, i32, f64, P, P, P, P]
         _lib.or_negative.argtypes = [i32, i32, i32, i64, P, P, P]
+        _lib.or_negative8.argtypes = [i32, i32, i32, i64, P, P, P]
+        _lib.or_cone8_of.argtypes = [i64, i64]
+        _lib.or_cone8_of.restype = C.c_int
         _lib.or_costmap.argtypes = [i64, P, P, P, P, P, P, P, P, P]
     return _lib
 
@@ -283,6 +286,20 @@ def negative(qs, defined, K, T_neg):
     return neg.reshape(ny, nx)
 
 
+def negative8(qs, defined, K, T_neg):
+    """O10 with 8 cones of half-angle 22.5 degrees (NEXT-3, reading B8)."""
+    ny, nx = qs.shape
+    neg = np.zeros(nx * ny, dtype=np.uint8)
+    lib().or_negative8(nx, ny, K, int(T_neg), _p(np.ascontiguousarray(qs, dtype=np.int32)),
+                       _p(np.ascontiguousarray(defined, dtype=np.uint8)), _p(neg))
+    return neg.reshape(ny, nx)
+
+
+def cone8_of(u: int, v: int) -> int:
+    """Index of the 8-cone holding offset (u, v); -1 if none or several."""
+    return int(lib().or_cone8_of(int(u), int(v)))
+
+
 def costmap(L: "Layers", weights) -> np.ndarray:
     """NEXT-4 costmap: weighted per-pixel sum of the layers (reading B5)."""
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float32).reshape(7))
@@ -353,7 +370,8 @@ class OracleMap:
                                  int(self.g["min_plane_points"]), ex)
         self._t("slope_roughness", t0)
         t0 = time.perf_counter()
-        neg = negative(qs, dfn, int(self.g["neg_obs_search_cells"]), self.T[3])
+        negf = negative8 if self.g.get("neg_8cone", False) else negative
+        neg = negf(qs, dfn, int(self.g["neg_obs_search_cells"]), self.T[3])
         self._t("negative", t0)
         spr = spread(self.dims, self.res, H, M1, M2)
         return Layers(height, dens, hard, soft, neg, sl, ro, qs, dfn, spr)
