@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
     ap.add_argument("--frames", type=int, default=4, help="distinct scans cycled")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--neg8cone", action="store_true",
+                    help="GVOM_FLAG_NEG_8CONE variant (8-cone negative-obstacle search)")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
     ap.add_argument("--slab", action="store_true",
                     help="multi-GPU slab partition of one frame (default for --config 4, N > 1)")
@@ -309,6 +311,9 @@ def main():
 
     from paper_2109_13176_b200 import GvomMap, LAYERS
     w = load_workload(args.config, args.frames, rank)
+    if args.neg8cone:
+        w.grid["neg_8cone"] = True
+        w.name += "+neg8cone"
     frames = w.frames
     npts = w.points_per_frame
     stream = torch.cuda.Stream(device=dev)

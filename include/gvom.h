@@ -66,6 +66,12 @@ typedef enum gvom_status {
 /* SPEC S:338 / SURVEY 8(f) NEXT-3 variant: hard and soft obstacle cells are
  * left out of every slope / roughness window (and get NaN themselves).    */
 #define GVOM_FLAG_SLOPE_SKIP_OBSTACLES 2
+/* SPEC S:327 / SURVEY 8(f) NEXT-3 variant: the negative-obstacle search uses
+ * 8 cones at j*45 degrees with half-angle 22.5 degrees (Chebyshev rings)
+ * instead of the paper's 4 axis cones (fig. 4); same decision rule.  The
+ * search tile needs about 6 (32 + 2K)^2 bytes of shared memory, so K <= 82
+ * (else GVOM_E_INVALID).                                                   */
+#define GVOM_FLAG_NEG_8CONE 4
 
 typedef struct gvom_config {
   int32_t nx, ny, nz;            /* voxels, each >= 1, nz <= 2048, nx*ny*nz < 2^31 */

@@ -60,7 +60,11 @@ bool valid_config(const gvom_config* c) {
   if ((int64_t)(c->neg_obs_search_cells + 3) << neg_qbits(c->nz) >= (1ll << 32)) return false;
   // the cone sweep's shared-memory ring holds at least two key lines
   if (!neg_sweep_fits(c->nx > c->ny ? c->nx : c->ny, c->neg_obs_search_cells)) return false;
-  if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES)) return false;
+  if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES | GVOM_FLAG_NEG_8CONE))
+    return false;
+  // the 8-cone search's tile (+ K halo) and prefix counts fit in shared memory
+  if ((c->flags & GVOM_FLAG_NEG_8CONE) && neg8_smem_bytes(c->neg_obs_search_cells) > kNegSmemMax)
+    return false;
   return true;
 }
 
@@ -394,6 +398,7 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.neg_cells = cfg->neg_obs_search_cells;
   h->lp.neg_qb = neg_qbits(cfg->nz);
   h->lp.skip_obstacles = (cfg->flags & GVOM_FLAG_SLOPE_SKIP_OBSTACLES) ? 1 : 0;
+  h->lp.neg_8cone = (cfg->flags & GVOM_FLAG_NEG_8CONE) ? 1 : 0;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
   bool ok = true;
@@ -593,10 +598,14 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
 static cudaError_t surface_layers(gvom_handle* h) {
   cudaError_t e = cudaEventRecord(h->ev_fork, h->ms());
   if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
-  if (e == cudaSuccess)
+  if (e == cudaSuccess && h->lp.neg_8cone) {
+    e = stage(h, GVOM_STAGE_NEGATIVE, true,
+              [&] { return launch_negative8(h->d, h->lp, h->layers, h->aux); }, h->aux);
+  } else if (e == cudaSuccess) {
     e = stage(h, GVOM_STAGE_NEGATIVE, true,
               [&] { return launch_negative(h->d, h->lp, h->layers, h->aux); }, h->aux);
-  if (e == cudaSuccess) h->launches++;  // k_neg_decide
+    if (e == cudaSuccess) h->launches++;  // k_neg_decide
+  }
   if (e == cudaSuccess)
     e = stage(
         h, GVOM_STAGE_SLOPE, true, [&] { return launch_slope(h->d, h->lp, h->layers, h->ms()); },

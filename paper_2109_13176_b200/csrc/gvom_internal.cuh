@@ -72,6 +72,7 @@ struct LayerParams {
   int64_t o_z;
   int32_t slope_window, min_plane_points, neg_cells;
   int32_t skip_obstacles;  // GVOM_FLAG_SLOPE_SKIP_OBSTACLES
+  int32_t neg_8cone;       // GVOM_FLAG_NEG_8CONE
   int32_t neg_qb;          // q_s < 2^neg_qb (= 16 + ceil(log2 nz)); see neg_keys
 };
 
@@ -107,6 +108,12 @@ inline size_t neg_slot_bytes(int B, int K) { return 8 * (size_t)neg_line_stride(
 inline size_t neg_state_bytes(int B, int K) { return 16 * ((size_t)B + 2 * (size_t)K + 2); }
 inline bool neg_sweep_fits(int B, int K) {
   return neg_state_bytes(B, K) + 2 * neg_slot_bytes(B, K) <= kNegSmemMax;
+}
+// k_negative8 (GVOM_FLAG_NEG_8CONE): a tile (16 or 32 cells square) + K halo
+// of q_s (int32), its summed-area table of defined cells (u16) and t_k (u8)
+inline size_t neg8_smem_bytes(int K, int tile = 32) {
+  const size_t W = (size_t)tile + 2 * (size_t)K, W1 = W + 1;
+  return ((4 * W * W + 2 * W1 * W1 + (size_t)K + 1) + 15) & ~(size_t)15;
 }
 
 // ---- launchers (each launches exactly one kernel; returns cudaError_t) ----
@@ -149,6 +156,8 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
                          cudaStream_t st);
 cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
                             const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st);
+cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                             cudaStream_t st);  // 8-cone variant -> neg directly
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
                            const LayerPtrs& out, cudaStream_t st, int64_t cbeg = 0,
                            int64_t cend = -1);

@@ -514,6 +514,120 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   }
 }
 
+// O10 with 8 cones (NEXT-3, reading B8): direct search per
+// undefined cell (one thread each) over a shared-memory tile of q_s with a
+// K-cell halo.  Ring k of the cone at j*45 degrees, in the cone's canonical
+// frame (unit vectors a = R^(j/2) (1,0) and b = R^(j/2) (0,1), R the +90
+// degree turn):
+//   even j: (k, t), |t| <= t_k       (t_k = max t with (t + k)^2 < 2 k^2)
+//   odd j : (u, k), t_k < u <= k  and  (k, v), t_k < v < k
+// -- straight segments, so whether a ring holds a defined cell is one or two
+// O(1) queries on a summed-area table of defined cells; only the first
+// non-empty ring of a cone is scanned for its min / max, and a cell with no
+// defined cell in its whole (2K+1)^2 square is settled by one query.  (The 8
+// rings together are the Chebyshev ring of 8k cells; the oracle tests cone
+// membership cell by cell instead.)
+__device__ __forceinline__ int neg8_tk(int k) {
+  int t = (int)(0.41421356f * (float)k);
+  while ((int64_t)(t + 1 + k) * (t + 1 + k) < 2ll * k * k) ++t;
+  while (t > 0 && (int64_t)(t + k) * (t + k) >= 2ll * k * k) --t;
+  return t;
+}
+
+template <int kTile>
+__global__ void __launch_bounds__(kTile * kTile) k_negative8(const Dims d, const LayerParams lp,
+                                                             const LayerPtrs out) {
+  extern __shared__ __align__(16) int32_t tq[];  // [W][W] q_s of tile + halo
+  const int K = lp.neg_cells;
+  const int W = kTile + 2 * K, W1 = W + 1;
+  uint16_t* sat = reinterpret_cast<uint16_t*>(tq + W * W);  // [W1][W1] summed-area table
+  uint8_t* tkt = reinterpret_cast<uint8_t*>(sat + W1 * W1);  // t_k, k = 0..K
+  const int nthr = kTile * kTile;
+  const int gx0 = blockIdx.x * kTile - K, gy0 = blockIdx.y * kTile - K;
+  for (int i = threadIdx.x; i < W * W; i += nthr) {
+    const int yy = gy0 + i / W, xx = gx0 + i % W;
+    tq[i] = ((unsigned)xx < (unsigned)d.nx && (unsigned)yy < (unsigned)d.ny)
+                ? __ldg(out.qs + xx + (int64_t)d.nx * yy)
+                : kQsUndef;
+  }
+  for (int k = threadIdx.x; k <= K; k += nthr) tkt[k] = (uint8_t)neg8_tk(k);
+  __syncthreads();
+  // sat[y][x] = defined cells in [0, x) x [0, y): row prefixes, then columns
+  for (int r = threadIdx.x; r < W1; r += nthr) {
+    uint16_t n = 0;
+    sat[r * W1] = 0;
+    for (int x = 0; x < W; ++x) {
+      if (r > 0) n += tq[(r - 1) * W + x] != kQsUndef;
+      sat[r * W1 + x + 1] = n;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < W1; c += nthr)
+    for (int y = 1; y < W1; ++y) sat[y * W1 + c] += sat[(y - 1) * W1 + c];
+  __syncthreads();
+  // defined cells in the tile-coordinate rectangle spanned by two corners
+  auto rect = [&](int x1, int y1, int x2, int y2) -> int {
+    const int lx = min(x1, x2), hx = max(x1, x2) + 1, ly = min(y1, y2), hy = max(y1, y2) + 1;
+    return (int)sat[hy * W1 + hx] - sat[hy * W1 + lx] - sat[ly * W1 + hx] + sat[ly * W1 + lx];
+  };
+  auto seg_minmax = [&](int x1, int y1, int sx, int sy, int n, int32_t& mn, int32_t& mx) {
+    for (int i = 0; i < n; ++i) {
+      const int32_t q = tq[(y1 + i * sy) * W + (x1 + i * sx)];
+      if (q != kQsUndef) {
+        mn = min(mn, q);
+        mx = max(mx, q);
+      }
+    }
+  };
+  const int tx = threadIdx.x % kTile, ty = threadIdx.x / kTile;
+  const int x = blockIdx.x * kTile + tx, y = blockIdx.y * kTile + ty;
+  if (x >= d.nx || y >= d.ny) return;
+  const int cx = tx + K, cy = ty + K;
+  const int64_t c = x + (int64_t)d.nx * y;
+  if (tq[cy * W + cx] != kQsUndef || rect(cx - K, cy - K, cx + K, cy + K) == 0) {
+    out.neg[c] = 0;  // defined, or nothing within reach of any cone
+    return;
+  }
+  int32_t mn = INT32_MAX, mx = INT32_MIN;
+  for (int j = 0; j < 8; ++j) {
+    int ax = 1, ay = 0, bx = 0, by = 1;
+    for (int m = 0; m < j / 2; ++m) {
+      const int t0 = ax;
+      ax = -ay;
+      ay = t0;
+      const int t1 = bx;
+      bx = -by;
+      by = t1;
+    }
+    for (int k = 1; k <= K; ++k) {
+      const int tk = tkt[k];
+      if (!(j & 1)) {  // (k, t), |t| <= tk: along b
+        const int px = cx + k * ax - tk * bx, py = cy + k * ay - tk * by;
+        const int qx = cx + k * ax + tk * bx, qy = cy + k * ay + tk * by;
+        if (rect(px, py, qx, qy) > 0) {
+          seg_minmax(px, py, bx, by, 2 * tk + 1, mn, mx);
+          break;
+        }
+      } else {  // (u, k), tk < u <= k along a; (k, v), tk < v < k along b
+        const int p1x = cx + (tk + 1) * ax + k * bx, p1y = cy + (tk + 1) * ay + k * by;
+        const int q1x = cx + k * ax + k * bx, q1y = cy + k * ay + k * by;
+        const int n1 = k - tk, n2 = k - 1 - tk;
+        const int p2x = cx + k * ax + (tk + 1) * bx, p2y = cy + k * ay + (tk + 1) * by;
+        const int q2x = cx + k * ax + (k - 1) * bx, q2y = cy + k * ay + (k - 1) * by;
+        const int c1 = rect(p1x, p1y, q1x, q1y);
+        const int c2 = n2 > 0 ? rect(p2x, p2y, q2x, q2y) : 0;
+        if (c1 + c2 > 0) {
+          seg_minmax(p1x, p1y, ax, ay, n1, mn, mx);
+          if (n2 > 0) seg_minmax(p2x, p2y, bx, by, n2, mn, mx);
+          break;
+        }
+      }
+    }
+  }
+  // reading B2: max - min > T_neg >= 0 implies two found cells
+  out.neg[c] = (mx != INT32_MIN && (int64_t)mx - (int64_t)mn > lp.T_neg) ? 1 : 0;
+}
+
 // O10 decision from the cone sweeps' min / max: undefined cell and
 // max F - min F > T_neg (T_neg >= 0, so this implies |F| >= 2, reading B2)
 __global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerParams lp,
@@ -693,6 +807,33 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_neg_decide<<<cells_blocks(d, 256), 256, 0, st>>>(d, lp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                             cudaStream_t st) {
+  // 32 x 32 tiles (1024 threads) when they give at least two blocks per SM,
+  // else 16 x 16 (more blocks for small maps, more halo per cell)
+  const int64_t t32 = ((d.nx + 31) / 32) * (int64_t)((d.ny + 31) / 32);
+  const int tile = t32 >= 2 * 148 ? 32 : 16;
+  const size_t smem = neg8_smem_bytes(lp.neg_cells, tile);
+  if (smem > kNegSmemMax) return cudaErrorInvalidConfiguration;
+  const dim3 grid((unsigned)((d.nx + tile - 1) / tile), (unsigned)((d.ny + tile - 1) / tile));
+  if (tile == 32) {
+    if (smem > 48 * 1024) {
+      const cudaError_t e = cudaFuncSetAttribute(
+          k_negative8<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_negative8<32><<<grid, 1024, smem, st>>>(d, lp, out);
+  } else {
+    if (smem > 48 * 1024) {
+      const cudaError_t e = cudaFuncSetAttribute(
+          k_negative8<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_negative8<16><<<grid, 256, smem, st>>>(d, lp, out);
+  }
   return cudaGetLastError();
 }
 

@@ -132,8 +132,9 @@ def make_config(grid: dict, max_points_per_frame: int) -> Config:
     c.res = float(grid["res"])
     c.z_center_frac = float(grid.get("z_center_frac", 0.5))
     c.buffer_frames = int(grid.get("buffer_frames", 8))
-    c.flags = (1 if grid.get("pipeline", False) else 0) | (  # GVOM_FLAG_PIPELINE
-        2 if grid.get("slope_skip_obstacles", False) else 0)  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES
+    c.flags = ((1 if grid.get("pipeline", False) else 0)  # GVOM_FLAG_PIPELINE
+               | (2 if grid.get("slope_skip_obstacles", False) else 0)  # ..._SLOPE_SKIP_OBSTACLES
+               | (4 if grid.get("neg_8cone", False) else 0))  # GVOM_FLAG_NEG_8CONE
     c.max_points_per_frame = int(max_points_per_frame)
     c.min_obstacle_height = float(grid["min_obstacle_height"])
     c.max_obstacle_height = float(grid["max_obstacle_height"])

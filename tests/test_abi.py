@@ -78,6 +78,12 @@ def test_cone_search_limits(lib):
     g = synth.grid_cfg(8192, 8, 8, 0.25)
     g["neg_obs_search_cells"] = 8
     assert gvom.workspace_bytes(g, 10) == 0
+    # GVOM_FLAG_NEG_8CONE: the search tile (32 + 2K)^2 and its summed-area table fit in smem
+    g = synth.grid_cfg(64, 64, 16, 0.25)
+    g["neg_8cone"] = True
+    for K, ok in ((82, True), (83, False)):
+        g["neg_obs_search_cells"] = K
+        assert (gvom.workspace_bytes(g, 10) > 0) == ok, K
 
 
 def test_create_rejects_bad_arguments(lib):

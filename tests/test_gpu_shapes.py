@@ -60,3 +60,25 @@ def test_slope_skip_obstacles_flag():
     grid["slope_skip_obstacles"] = True
     w, frames = _world_frames(3, 0.3, 77)
     run_sequence(synth.Workload("skip_obstacles", grid, frames, w))
+
+
+@pytest.mark.parametrize("case", [0, 1, 3])
+def test_neg_8cone_flag_shapes(case):
+    # GVOM_FLAG_NEG_8CONE (SPEC S:327 / NEXT-3 variant, reading B8) against
+    # or_negative8: odd shapes, K = 3 .. 24 cone distances, tiles straddling edges
+    nx, ny, nz, res, K, over = CASES[case]
+    grid = synth.grid_cfg(nx, ny, nz, res, buffer_frames=K)
+    grid.update(over)
+    grid["neg_8cone"] = True
+    w, frames = _world_frames(3, 0.41 + 0.1 * case, 300 + case)
+    run_sequence(synth.Workload(f"neg8_{case}", grid, frames, w))
+
+
+def test_neg_8cone_flag_c2_and_c4():
+    # the shipped workloads (K = 24 and 30 cone cells) with the 8-cone search
+    for i in (1, 3):
+        wl = synth.workload(i)
+        grid = dict(wl.grid)
+        grid["neg_8cone"] = True
+        run_sequence(synth.Workload(wl.name + "_neg8", grid, wl.frames, wl.world),
+                     check_merged=False)
