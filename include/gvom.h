@@ -189,7 +189,9 @@ GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAY
                                         const size_t dst_bytes[GVOM_LAYER_COUNT]);
 
 /* One scan end to end: gvom_shift + gvom_integrate_scan + gvom_compute_maps
- * (+ gvom_export_layers when dst != NULL), same arguments, results and
+ * (+ gvom_export_layers when dst != NULL; + the costmap into cost_dst when
+ * cost_weights != NULL, fused with the export as in gvom_export_layers_cost;
+ * cost_weights and cost_dst are both NULL or both set), same arguments, results and
  * errors as those calls in sequence (inputs are validated before anything is
  * enqueued).  The frame's kernels are captured on the handle's stream and run
  * as ONE CUDA graph launch: the cached executable graph is patched with the
@@ -202,6 +204,7 @@ GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAY
 GVOM_API gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,
                                int32_t n_scans, void* const dst[GVOM_LAYER_COUNT],
                                const size_t dst_bytes[GVOM_LAYER_COUNT],
+                               const float cost_weights[7], void* cost_dst, size_t cost_bytes,
                                int64_t out_delta_voxels[3]);
 
 /* gvom_step counters: out[0] graph launches, out[1] graph instantiations,
@@ -216,6 +219,16 @@ GVOM_API gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]);
  * dst: nx*ny float32, host or device; ordered on the map stream.          */
 GVOM_API gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst,
                                   size_t dst_bytes);
+
+/* gvom_export_layers + gvom_costmap in ONE pass (NEXT-4 "fused into
+ * export"): every layer cell is read once, written to dst[l] and folded into
+ * the cost (same formula and order as gvom_costmap).  One kernel when every
+ * destination is 4-byte aligned device memory; otherwise the two calls in
+ * sequence.  Errors as those calls.                                        */
+GVOM_API gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
+                                             const size_t dst_bytes[GVOM_LAYER_COUNT],
+                                             const float weights[7], void* cost_dst,
+                                             size_t cost_bytes);
 
 /* World-voxel origin of the last compute_maps (newest buffer map).  */
 GVOM_API gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]);

@@ -687,9 +687,16 @@ gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT]
 // or instantiated anew, and launched as one graph.
 gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,
                       int32_t n_scans, void* const dst[GVOM_LAYER_COUNT],
-                      const size_t dst_bytes[GVOM_LAYER_COUNT], int64_t out_delta[3]) {
+                      const size_t dst_bytes[GVOM_LAYER_COUNT], const float cost_weights[7],
+                      void* cost_dst, size_t cost_bytes, int64_t out_delta[3]) {
   if (!h || !vehicle_xyz) return GVOM_E_INVALID;
   if (dst && !dst_bytes) return GVOM_E_INVALID;
+  if ((cost_weights == nullptr) != (cost_dst == nullptr)) return GVOM_E_INVALID;
+  if (cost_weights) {
+    for (int i = 0; i < 7; ++i)
+      if (!isfinite(cost_weights[i])) return GVOM_E_INVALID;
+    if (cost_bytes < 4 * (size_t)h->lay.cells) return GVOM_E_SIZE;
+  }
   if (dst)
     for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
       size_t elem;
@@ -720,7 +727,12 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
   auto frame = [&]() -> gvom_status {
     gvom_status s = gvom_integrate_scan(h, scans, n_scans);
     if (s == GVOM_OK) s = gvom_compute_maps(h);
-    if (s == GVOM_OK && dst) s = gvom_export_layers(h, dst, dst_bytes);
+    if (s == GVOM_OK && dst && cost_weights)
+      s = gvom_export_layers_cost(h, dst, dst_bytes, cost_weights, cost_dst, cost_bytes);
+    else if (s == GVOM_OK && dst)
+      s = gvom_export_layers(h, dst, dst_bytes);
+    else if (s == GVOM_OK && cost_weights)
+      s = gvom_costmap(h, cost_weights, cost_dst, cost_bytes);
     return s;
   };
   if (!graph) {
@@ -801,6 +813,39 @@ gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst, size
       [&] { return launch_costmap(h->d, h->layers, cw, out, h->ms()); }, h->ms()));
   if (!direct)
     GVOM_CU(cudaMemcpyAsync(dst, out, bytes, cudaMemcpyDefault, h->ms()));
+  return GVOM_OK;
+}
+
+gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
+                                   const size_t dst_bytes[GVOM_LAYER_COUNT],
+                                   const float weights[7], void* cost_dst, size_t cost_bytes) {
+  if (!h || !dst || !dst_bytes || !weights || !cost_dst) return GVOM_E_INVALID;
+  if (!h->maps_valid) return GVOM_E_EMPTY;
+  CostWeights cw;
+  for (int i = 0; i < 7; ++i) {
+    if (!isfinite(weights[i])) return GVOM_E_INVALID;
+    cw.w[i] = weights[i];
+  }
+  if (cost_bytes < 4 * (size_t)h->lay.cells) return GVOM_E_SIZE;
+  CopyJob job;
+  bool fused = is_device_ptr(cost_dst) && ((uintptr_t)cost_dst & 3) == 0;
+  for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
+    size_t elem;
+    job.src[l] = layer_src(h, l, &elem);
+    job.dst[l] = dst[l];
+    job.bytes[l] = (int64_t)(elem * (size_t)h->lay.cells);
+    if (!dst[l]) return GVOM_E_INVALID;
+    if (dst_bytes[l] < (size_t)job.bytes[l]) return GVOM_E_SIZE;
+    if (((uintptr_t)dst[l] & 3) != 0 || !is_device_ptr(dst[l])) fused = false;
+  }
+  if (!fused) {  // host (or unaligned) destinations: copies + the costmap kernel
+    const gvom_status s = gvom_export_layers(h, dst, dst_bytes);
+    return s != GVOM_OK ? s : gvom_costmap(h, weights, cost_dst, cost_bytes);
+  }
+  GVOM_CU(stage(
+      h, GVOM_STAGE_EXPORT, true,
+      [&] { return launch_export_cost(h->d, h->layers, job, cw, (float*)cost_dst, h->ms()); },
+      h->ms()));
   return GVOM_OK;
 }
 

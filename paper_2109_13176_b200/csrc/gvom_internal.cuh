@@ -200,6 +200,9 @@ cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st);
 struct CostWeights {
   float w[7];  // hard, soft, density, negative, slope, roughness, unknown
 };
+// all layers to job.dst (device, 4-byte aligned) + the costmap, one pass
+cudaError_t launch_export_cost(const Dims& d, const LayerPtrs& in, const CopyJob& job,
+                               const CostWeights& cw, float* cost, cudaStream_t st);
 cudaError_t launch_costmap(const Dims& d, const LayerPtrs& in, const CostWeights& cw, float* out,
                            cudaStream_t st);
 

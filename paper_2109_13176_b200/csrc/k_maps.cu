@@ -644,22 +644,49 @@ __global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerPar
 // Costmap: weighted per-pixel sum of the layers,
 // f32 RN in the order hard, soft, density, negative, slope, roughness,
 // unknown; an undefined (NaN) layer contributes 0 (reading B5).
-__global__ void __launch_bounds__(256) k_costmap(const Dims d, const LayerPtrs in,
-                                                 const CostWeights cw, float* __restrict__ out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)d.nx * d.ny) return;
-  const float h = __ldg(in.height + c), de = __ldg(in.density + c);
-  const float sl = __ldg(in.slope + c), ro = __ldg(in.rough + c);
-  const uint8_t ng = __ldg(in.neg + c);
+__device__ __forceinline__ float cost_of(const CostWeights& cw, float h, float de, uint8_t hd,
+                                         uint8_t so, uint8_t ng, float sl, float ro) {
   float acc = 0.0f;
-  acc = __fadd_rn(acc, __fmul_rn(cw.w[0], (float)__ldg(in.hard + c)));
-  acc = __fadd_rn(acc, __fmul_rn(cw.w[1], (float)__ldg(in.soft + c)));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[0], (float)hd));
+  acc = __fadd_rn(acc, __fmul_rn(cw.w[1], (float)so));
   acc = __fadd_rn(acc, __fmul_rn(cw.w[2], isnan(de) ? 0.0f : de));
   acc = __fadd_rn(acc, __fmul_rn(cw.w[3], (float)ng));
   acc = __fadd_rn(acc, __fmul_rn(cw.w[4], isnan(sl) ? 0.0f : sl));
   acc = __fadd_rn(acc, __fmul_rn(cw.w[5], isnan(ro) ? 0.0f : ro));
   acc = __fadd_rn(acc, __fmul_rn(cw.w[6], (isnan(h) && !ng) ? 1.0f : 0.0f));
-  out[c] = acc;
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_costmap(const Dims d, const LayerPtrs in,
+                                                 const CostWeights cw, float* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)d.nx * d.ny) return;
+  out[c] = cost_of(cw, __ldg(in.height + c), __ldg(in.density + c), __ldg(in.hard + c),
+                   __ldg(in.soft + c), __ldg(in.neg + c), __ldg(in.slope + c),
+                   __ldg(in.rough + c));
+}
+
+// Export fused with the costmap (NEXT-4 "fused into export"): each layer
+// cell is read once, written to its destination and folded into the cost.
+// Destinations in GVOM_LAYER order.
+__global__ void __launch_bounds__(256) k_export_cost(const Dims d, const LayerPtrs in,
+                                                     const __grid_constant__ CopyJob job,
+                                                     const CostWeights cw,
+                                                     float* __restrict__ cost) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)d.nx * d.ny) return;
+  const float h = __ldcs(in.height + c), de = __ldcs(in.density + c);
+  const uint8_t hd = __ldcs(in.hard + c), so = __ldcs(in.soft + c), ng = __ldcs(in.neg + c);
+  const float sl = __ldcs(in.slope + c), ro = __ldcs(in.rough + c), sp = __ldcs(in.spread + c);
+  static_cast<float*>(job.dst[GVOM_LAYER_HEIGHT])[c] = h;
+  static_cast<float*>(job.dst[GVOM_LAYER_DENSITY])[c] = de;
+  static_cast<uint8_t*>(job.dst[GVOM_LAYER_HARD])[c] = hd;
+  static_cast<uint8_t*>(job.dst[GVOM_LAYER_SOFT])[c] = so;
+  static_cast<uint8_t*>(job.dst[GVOM_LAYER_NEGATIVE])[c] = ng;
+  static_cast<float*>(job.dst[GVOM_LAYER_SLOPE])[c] = sl;
+  static_cast<float*>(job.dst[GVOM_LAYER_ROUGHNESS])[c] = ro;
+  static_cast<float*>(job.dst[GVOM_LAYER_SPREAD])[c] = sp;
+  cost[c] = cost_of(cw, h, de, hd, so, ng, sl, ro);
 }
 
 // merged occupancy bits of the combined map (export path)
@@ -850,6 +877,12 @@ cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st) {
 cudaError_t launch_costmap(const Dims& d, const LayerPtrs& in, const CostWeights& cw, float* out,
                            cudaStream_t st) {
   k_costmap<<<cells_blocks(d, 256), 256, 0, st>>>(d, in, cw, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export_cost(const Dims& d, const LayerPtrs& in, const CopyJob& job,
+                               const CostWeights& cw, float* cost, cudaStream_t st) {
+  k_export_cost<<<cells_blocks(d, 256), 256, 0, st>>>(d, in, job, cw, cost);
   return cudaGetLastError();
 }
 

@@ -91,7 +91,8 @@ def load_library() -> C.CDLL:
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
         "gvom_export_layers": ([P, P, P], I32),
-        "gvom_step": ([P, P, P, I32, P, P, P], I32),
+        "gvom_step": ([P, P, P, I32, P, P, P, P, C.c_size_t, P], I32),
+        "gvom_export_layers_cost": ([P, P, P, P, P, C.c_size_t], I32),
         "gvom_graph_stats": ([P, P], I32),
         "gvom_map_origin": ([P, P], I32),
         "gvom_export_voxels": ([P, P, P, I64, P], I32),
@@ -123,7 +124,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
-            "gvom_step", "gvom_graph_stats")
+            "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -316,24 +317,49 @@ class GvomMap:
                                              for n in LAYERS])
         return res, ptrs, sizes
 
-    def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None) -> Dict[str, torch.Tensor]:
+    def _cost_dst(self, weights, cost):
+        w = (C.c_float * 7)(*[float(v) for v in weights])
+        if cost is None:
+            cost = torch.empty((self.ny, self.nx), dtype=torch.float32, device=self.device)
+        assert cost.is_contiguous() and cost.dtype == torch.float32
+        return w, cost
+
+    def export_layers(self, out: Optional[Dict[str, torch.Tensor]] = None,
+                      cost_weights=None, cost: Optional[torch.Tensor] = None
+                      ) -> Dict[str, torch.Tensor]:
         """All layers with one gvom_export_layers call (one kernel when every
-        destination is device memory)."""
+        destination is device memory); with cost_weights also the costmap,
+        fused into the same pass (gvom_export_layers_cost), as key "cost"."""
         res, ptrs, sizes = self._layer_dst(out)
-        _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
+        if cost_weights is None:
+            _check(self.lib.gvom_export_layers(self.h, ptrs, sizes), "gvom_export_layers")
+            return res
+        w, cost = self._cost_dst(cost_weights, cost)
+        _check(self.lib.gvom_export_layers_cost(self.h, ptrs, sizes, w, C.c_void_p(cost.data_ptr()),
+                                                cost.numel() * 4), "gvom_export_layers_cost")
+        res["cost"] = cost
         return res
 
     def step(self, vehicle_xyz: Sequence[float], scans: Iterable[ScanLike],
-             out: Optional[Dict[str, torch.Tensor]] = None, export: bool = True):
+             out: Optional[Dict[str, torch.Tensor]] = None, export: bool = True,
+             cost_weights=None, cost: Optional[torch.Tensor] = None):
         """gvom_step: shift + integrate_scan + compute_maps (+ export of all
-        layers into `out`, allocated if None) as one CUDA graph launch.
+        layers into `out`, allocated if None; + the costmap with cost_weights,
+        as key "cost") as one CUDA graph launch.
         Returns (shift delta, layers or None)."""
         p = (C.c_double * 3)(*[float(v) for v in vehicle_xyz])
         dlt = (C.c_int64 * 3)()
         arr, n, keep = self._scan_array(scans)
         res, ptrs, sizes = self._layer_dst(out) if export else (None, None, None)
-        _check(self.lib.gvom_step(self.h, p, arr, n, ptrs, sizes, dlt), "gvom_step")
+        w, cp, cb = None, None, 0
+        if cost_weights is not None:
+            w, cost = self._cost_dst(cost_weights, cost)
+            cp, cb = C.c_void_p(cost.data_ptr()), cost.numel() * 4
+        _check(self.lib.gvom_step(self.h, p, arr, n, ptrs, sizes, w, cp, cb, dlt), "gvom_step")
         self._keep.append(keep)
+        if cost_weights is not None:
+            res = {} if res is None else res
+            res["cost"] = cost
         return np.array(dlt[:], dtype=np.int64), res
 
     def graph_stats(self) -> dict:

@@ -218,3 +218,37 @@ def test_costmap_matches_oracle(c2):
         tol = 1e-4 * (1.0 + float(np.abs(w).sum()))
         assert np.allclose(got.cpu().numpy(), ref, rtol=1e-5, atol=tol)
         assert np.array_equal(got.cpu().numpy(), host.numpy())
+
+
+def test_costmap_fused_into_export_and_step(c2):
+    # NEXT-4 "fused into export": gvom_export_layers_cost (one pass) and
+    # gvom_step with cost weights (inside the step graph) give the layers and
+    # the same cost as the separate calls, and match the oracle
+    f = c2.frames[0]
+    m = GvomMap(c2.grid, max_points_per_frame=f.n_points)
+    om = O.OracleMap(c2.grid)
+    om.shift(f.vehicle_xyz)
+    om.integrate([(s.points, s.pose) for s in f.scans])
+    L = om.compute_maps()
+    w = np.array([5.0, 2.0, 1.5, 4.0, 3.0, 7.0, 0.5], np.float32)
+    _, lay = m.step(f.vehicle_xyz, [to_dev(s) for s in f.scans], cost_weights=w)
+    m.synchronize()
+    assert m.graph_stats()["graph_launches"] == 1
+    got = {k: v.cpu().numpy() for k, v in lay.items()}
+    compare_layers(got, L)
+    tol = 1e-4 * (1.0 + float(np.abs(w).sum()))
+    assert np.allclose(got["cost"], O.costmap(L, w), rtol=1e-5, atol=tol)
+    # the fused pass is bit-identical to the separate costmap kernel
+    sep = m.costmap(w)
+    fused = m.export_layers(cost_weights=w)
+    m.synchronize()
+    assert np.array_equal(sep.cpu().numpy(), got["cost"])
+    assert np.array_equal(fused["cost"].cpu().numpy(), got["cost"])
+    # host destinations take the unfused path, same values
+    host = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in lay.items()
+            if k != "cost"}
+    hc = torch.empty(got["cost"].shape, dtype=torch.float32).pin_memory()
+    m.export_layers(host, cost_weights=w, cost=hc)
+    m.synchronize()
+    assert np.array_equal(hc.numpy(), got["cost"])
+    compare_layers({k: v.numpy() for k, v in host.items()}, L)
