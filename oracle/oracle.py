@@ -312,6 +312,28 @@ def costmap(L: "Layers", weights) -> np.ndarray:
     return out
 
 
+def roll_window(dims, acc, d):
+    """NEXT-3 rolling map (reading B9): re-centre the accumulated dense map
+    (H, Mi, mn, M1, M2 over the window, L order) on an origin moved by d
+    voxels.  World voxel o_new + l was o_old + (l + d): the overlap is kept,
+    voxels that left the window are dropped, entering voxels start empty."""
+    nx, ny, nz = dims
+    out = []
+    for a, empty in zip(acc, (0, 0, 0xFFFFFFFF, 0, 0)):
+        src = a.reshape(ny, nx, nz)
+        dst = np.full_like(src, empty)
+        sl_new, sl_old = [], []
+        for dd, n in ((int(d[1]), ny), (int(d[0]), nx), (int(d[2]), nz)):
+            lo, hi = max(0, -dd), min(n, n - dd)  # new logical range that was inside
+            if lo >= hi:
+                lo = hi = 0
+            sl_new.append(slice(lo, hi))
+            sl_old.append(slice(lo + dd, hi + dd))
+        dst[tuple(sl_new)] = src[tuple(sl_old)]
+        out.append(dst.reshape(-1))
+    return tuple(out)
+
+
 # --------------------------------------------------------------------------
 # the whole update, same call sequence as the C-ABI
 # --------------------------------------------------------------------------
@@ -328,6 +350,12 @@ class OracleMap:
         self.buffer: List[FrameMap] = []
         self.times: Dict[str, float] = {}
         self.merged = None
+        # NEXT-3 rolling map (reading B9): one accumulated window, K = infinity
+        self.rolling = bool(grid.get("rolling", False))
+        V = self.dims[0] * self.dims[1] * self.dims[2]
+        self.roll = (np.zeros(V, np.uint64), np.zeros(V, np.uint64),
+                     np.full(V, 0xFFFFFFFF, np.uint32), np.zeros(V, np.uint64),
+                     np.zeros(V, np.uint64)) if self.rolling else None
 
     def _t(self, key, t0):
         self.times[key] = self.times.get(key, 0.0) + (time.perf_counter() - t0)
@@ -337,6 +365,8 @@ class OracleMap:
         o = snap_origin(*self.dims, self.res, self.g.get("z_center_frac", 0.5), vehicle_xyz)
         d = o - self.origin
         self.origin = o
+        if self.rolling and np.any(d != 0):
+            self.roll = roll_window(self.dims, self.roll, d)
         self._t("shift", t0)
         return d
 
@@ -351,14 +381,23 @@ class OracleMap:
         self.buffer.append(fm)
         if len(self.buffer) > self.K:
             self.buffer.pop(0)
+        if self.rolling:  # B9: the frame's counts join the window map
+            H, Mi, MN, M1, M2 = self.roll
+            self.roll = (H + h.astype(np.uint64), Mi + m.astype(np.uint64),
+                         np.minimum(MN, mn.astype(np.uint32)), M1 + m1, M2 + m2)
+            self.roll_frames = getattr(self, "roll_frames", 0) + 1
         return fm
 
     def compute_maps(self) -> Layers:
         if not self.buffer:
             raise RuntimeError("empty buffer")
-        o = self.buffer[-1].origin  # the newest buffer map's origin
         t0 = time.perf_counter()
-        H, Mi, mn, M1, M2 = combine(self.dims, self.buffer, o)
+        if self.rolling:  # B9: the accumulated window at the current origin
+            o = self.origin.copy()
+            H, Mi, mn, M1, M2 = self.roll
+        else:
+            o = self.buffer[-1].origin  # the newest buffer map's origin
+            H, Mi, mn, M1, M2 = combine(self.dims, self.buffer, o)
         self._t("combine", t0)
         self.merged = (H, Mi, mn, M1, M2, o.copy())
         t0 = time.perf_counter()
