@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -56,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--neg8cone", action="store_true",
                     help="GVOM_FLAG_NEG_8CONE variant (8-cone negative-obstacle search)")
+    ap.add_argument("--rolling", action="store_true",
+                    help="GVOM_FLAG_ROLLING variant (one accumulated window map, K = inf)")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
     ap.add_argument("--slab", action="store_true",
                     help="multi-GPU slab partition of one frame (default for --config 4, N > 1)")
@@ -292,6 +295,40 @@ def main_slab(args):
     return 0
 
 
+def pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier):
+    """integrate(t+1) overlaps compute_maps(t) + export(t); no L2 flush (a
+    flush would serialise the overlap), timed over the whole sequence."""
+    from paper_2109_13176_b200 import GvomMap
+    import torch
+    gp = dict(w.grid)
+    gp["pipeline"] = True
+    mp_ = GvomMap(gp, max_points_per_frame=npts, device=dev, stream=stream)
+    ms_ = mp_.map_stream
+
+    def pstep(i):
+        f = frames[i % len(frames)]
+        mp_.shift(f.vehicle_xyz)
+        mp_.integrate_scan(dev_frames[i % len(frames)])
+        mp_.compute_maps()
+        mp_.export_layers(out)
+
+    for i in range(args.warmup):
+        pstep(i)
+    mp_.synchronize()
+    barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(args.steps):
+        pstep(i)
+    b.record(ms_)
+    mp_.synchronize()
+    ms = a.elapsed_time(b)
+    del mp_
+    barrier()
+    return ms
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -314,6 +351,10 @@ def main():
     if args.neg8cone:
         w.grid["neg_8cone"] = True
         w.name += "+neg8cone"
+    if args.rolling:
+        w.grid["rolling"] = True
+        w.grid["buffer_frames"] = 1
+        w.name += "+rolling"
     frames = w.frames
     npts = w.points_per_frame
     stream = torch.cuda.Stream(device=dev)
@@ -407,34 +448,10 @@ def main():
         barrier()
 
         # ---- pipelined sustained sequence (GVOM_FLAG_PIPELINE) --------
-        # integrate(t+1) overlaps compute_maps(t) + export(t); no L2 flush (a
-        # flush would serialise the overlap), timed over the whole sequence
-        gp = dict(w.grid)
-        gp["pipeline"] = True
-        mp_ = GvomMap(gp, max_points_per_frame=npts, device=dev, stream=stream)
-        ms_ = mp_.map_stream
-
-        def pstep(i):
-            f = frames[i % len(frames)]
-            mp_.shift(f.vehicle_xyz)
-            mp_.integrate_scan(dev_frames[i % len(frames)])
-            mp_.compute_maps()
-            mp_.export_layers(out)
-
-        for i in range(args.warmup):
-            pstep(i)
-        mp_.synchronize()
-        barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for i in range(args.steps):
-            pstep(i)
-        b.record(ms_)
-        mp_.synchronize()
-        pipe_ms = a.elapsed_time(b)
-        del mp_
-        barrier()
+        # (not with the rolling map: GVOM_FLAG_ROLLING excludes pipelining)
+        pipe_ms = float("nan")
+        if not w.grid.get("rolling", False):
+            pipe_ms = pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier)
 
     t = torch.tensor([total_ms, e2e_ms, pipe_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -490,10 +507,11 @@ def main():
                            "separate calls without a graph)",
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * npts,
                     "d2h_bytes_per_step": m.nx * m.ny * (4 * 5 + 3), "steps": e2e_steps},
-            "pipelined": {"value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
-                          "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),
-                          "note": "GVOM_FLAG_PIPELINE: integrate(t+1) overlaps compute_maps(t); "
-                                  "sustained sequence, no L2 flush between steps"},
+            "pipelined": None if math.isnan(pipe_ms) else {
+                "value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
+                "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),
+                "note": "GVOM_FLAG_PIPELINE: integrate(t+1) overlaps compute_maps(t); "
+                        "sustained sequence, no L2 flush between steps"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

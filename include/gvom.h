@@ -72,6 +72,17 @@ typedef enum gvom_status {
  * search tile needs about 6 (32 + 2K)^2 bytes of shared memory, so K <= 82
  * (else GVOM_E_INVALID).                                                   */
 #define GVOM_FLAG_NEG_8CONE 4
+/* SURVEY 8(f) NEXT-3 variant, the rolling map (K = infinity; reading B9):
+ * instead of a buffer of K scan maps merged at every compute_maps, ONE window
+ * map accumulates every scan (u64 counts) since each voxel entered the
+ * window; gvom_shift moves the window, dropping the voxels that leave it and
+ * clearing the ones that enter it (stored toroidally in world voxel
+ * coordinates: only the entering slabs are written).  compute_maps uses the
+ * current window origin.  Requires buffer_frames == 1 (the scratch slot of
+ * the scan being integrated) and no GVOM_FLAG_PIPELINE; the slab calls and
+ * gvom_export_voxels are unavailable (GVOM_E_INVALID) -- see
+ * gvom_export_window.  Extra workspace: 36 bytes per voxel.                */
+#define GVOM_FLAG_ROLLING 8
 
 typedef struct gvom_config {
   int32_t nx, ny, nz;            /* voxels, each >= 1, nz <= 2048, nx*ny*nz < 2^31 */
@@ -158,7 +169,9 @@ GVOM_API gvom_status gvom_synchronize(gvom_handle* h);
  * vehicle"; P:81 origin "always an integer multiple of the map resolution").
  * o = floor(p/res + 0.5) - (nx/2, ny/2, floor(nz*z_center_frac)) voxels
  * (reading A3).  Sets the origin used by subsequent integrate_scan calls;
- * writes o_new - o_old to out_delta_voxels (may be NULL).  Host only.      */
+ * writes o_new - o_old to out_delta_voxels (may be NULL).  Host only, except
+ * with GVOM_FLAG_ROLLING, where it also enqueues the clearing of the
+ * entering slabs of the window map on the handle's stream.                */
 GVOM_API gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_delta_voxels[3]);
 
 /* Pointcloud processing: transform the scans of n_scans sensors into
@@ -229,6 +242,13 @@ GVOM_API gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVO
                                              const size_t dst_bytes[GVOM_LAYER_COUNT],
                                              const float weights[7], void* cost_dst,
                                              size_t cost_bytes);
+
+/* GVOM_FLAG_ROLLING only: the window map, dense in L order over the current
+ * window: hits, misses, m1, m2 (u64) and min_dz (u32, 0xFFFFFFFF where no
+ * return) per voxel, each a caller-owned device array of nx*ny*nz entries.
+ * GVOM_E_INVALID without the flag.  Stream-ordered.                       */
+GVOM_API gvom_status gvom_export_window(gvom_handle* h, uint64_t* d_hits, uint64_t* d_misses,
+                                        uint32_t* d_min_dz, uint64_t* d_m1, uint64_t* d_m2);
 
 /* World-voxel origin of the last compute_maps (newest buffer map).  */
 GVOM_API gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]);

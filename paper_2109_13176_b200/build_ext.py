@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libgvom.so")
-SOURCES = ["k_integrate.cu", "k_maps.cu", "k_slab.cu", "gvom_api.cu"]
+SOURCES = ["k_integrate.cu", "k_maps.cu", "k_slab.cu", "k_roll.cu", "gvom_api.cu"]
 HEADERS = ["gvom_internal.cuh"]
 
 NVCC_FLAGS = [

@@ -32,7 +32,7 @@ struct Slot {
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
   size_t staging, rank_tmp, rank_status, epcnt, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
-      total;
+      roll_rows, roll_nmn, roll_bits, total;
   int64_t cap, nblk, cells;
 };
 
@@ -60,7 +60,12 @@ bool valid_config(const gvom_config* c) {
   if ((int64_t)(c->neg_obs_search_cells + 3) << neg_qbits(c->nz) >= (1ll << 32)) return false;
   // the cone sweep's shared-memory ring holds at least two key lines
   if (!neg_sweep_fits(c->nx > c->ny ? c->nx : c->ny, c->neg_obs_search_cells)) return false;
-  if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES | GVOM_FLAG_NEG_8CONE))
+  if (c->flags & ~(GVOM_FLAG_PIPELINE | GVOM_FLAG_SLOPE_SKIP_OBSTACLES | GVOM_FLAG_NEG_8CONE |
+                   GVOM_FLAG_ROLLING))
+    return false;
+  // the rolling map replaces the buffer: one scratch frame slot, no pipelining
+  if ((c->flags & GVOM_FLAG_ROLLING) &&
+      (c->buffer_frames != 1 || (c->flags & GVOM_FLAG_PIPELINE)))
     return false;
   // the 8-cone search's tile (+ K halo) and prefix counts fit in shared memory
   if ((c->flags & GVOM_FLAG_NEG_8CONE) && neg8_smem_bytes(c->neg_obs_search_cells) > kNegSmemMax)
@@ -118,6 +123,14 @@ Layout make_layout(const gvom_config* c) {
   off += align_up(4 * (size_t)d.W);
   l.mprefix = off;
   off += align_up(4 * (size_t)d.W);
+  if (c->flags & GVOM_FLAG_ROLLING) {  // the window map (k_roll.cu)
+    l.roll_rows = off;  // hits, misses, m1, m2: four u64 arrays
+    off += 4 * align_up(8 * (size_t)d.V);
+    l.roll_nmn = off;
+    off += align_up(4 * (size_t)d.V);
+    l.roll_bits = off;
+    off += align_up(4 * (size_t)d.W);
+  }
   l.total = off;
   return l;
 }
@@ -169,6 +182,8 @@ struct gvom_handle {
   int64_t maps_calls = 0;           // compute_maps calls so far
   std::vector<int64_t> slot_reader; // last compute_maps call that read a slot
   // gvom_step: the frame's launches, captured and replayed as one CUDA graph
+  bool rolling = false;                // GVOM_FLAG_ROLLING: the window map
+  RollGrid roll{};
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap = nullptr;          // capture stream (the caller's may be legacy)
   bool capturing = false;              // inside gvom_step's capture
@@ -240,6 +255,17 @@ SensorParams sensor_params(const gvom_config& c, const double* P, const int64_t 
     sp.S[i] = (int32_t)floorf(sp.b[i]);
   }
   return sp;
+}
+
+// the rolling map's window origin and its per-axis physical offsets
+void roll_set_origin(RollGrid& g, const gvom_config& c, const int64_t o[3]) {
+  auto pm = [](int64_t a, int n) { return (int32_t)(((a % n) + n) % n); };
+  g.ox = o[0];
+  g.oy = o[1];
+  g.oz = o[2];
+  g.xo = pm(o[0], c.nx);
+  g.yo = pm(o[1], c.ny);
+  g.zo = pm(o[2], c.nz);
 }
 
 bool is_pinned_host_ptr(const void* p) {
@@ -401,6 +427,17 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.neg_8cone = (cfg->flags & GVOM_FLAG_NEG_8CONE) ? 1 : 0;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
+  h->rolling = (cfg->flags & GVOM_FLAG_ROLLING) != 0;
+  if (h->rolling) {  // all-zero workspace = the empty window map
+    const size_t a8 = align_up(8 * (size_t)h->d.V);
+    h->roll.hits = (uint64_t*)(h->ws + lay.roll_rows);
+    h->roll.misses = (uint64_t*)(h->ws + lay.roll_rows + a8);
+    h->roll.m1 = (uint64_t*)(h->ws + lay.roll_rows + 2 * a8);
+    h->roll.m2 = (uint64_t*)(h->ws + lay.roll_rows + 3 * a8);
+    h->roll.nmn = (uint32_t*)(h->ws + lay.roll_nmn);
+    h->roll.bits = (uint32_t*)(h->ws + lay.roll_bits);
+    roll_set_origin(h->roll, h->cfg, h->origin);
+  }
   bool ok = true;
   if (h->pipelined) {
     ok = cudaStreamCreateWithFlags(&h->mst, cudaStreamNonBlocking) == cudaSuccess &&
@@ -460,6 +497,19 @@ gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_
   snap(h->cfg, vehicle_xyz, o);
   if (out_delta)
     for (int i = 0; i < 3; ++i) out_delta[i] = o[i] - h->origin[i];
+  if (h->rolling) {
+    // the window moves: clear the slabs that enter it (reading B9)
+    const int n[3] = {h->cfg.nx, h->cfg.ny, h->cfg.nz};
+    roll_set_origin(h->roll, h->cfg, o);
+    for (int a = 0; a < 3; ++a) {
+      const int64_t dlt = o[a] - h->origin[a];
+      if (dlt == 0) continue;
+      const int cnt = (int)(dlt > 0 ? (dlt < n[a] ? dlt : n[a]) : (-dlt < n[a] ? -dlt : n[a]));
+      const int64_t w0 = dlt > 0 ? o[a] + n[a] - cnt : o[a];
+      GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true,
+                    [&] { return launch_roll_clear(h->roll, h->d, a, w0, cnt, h->st); }));
+    }
+  }
   for (int i = 0; i < 3; ++i) h->origin[i] = o[i];
   return GVOM_OK;
 }
@@ -587,6 +637,10 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     }));
   }
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
+  if (h->rolling)  // the frame map joins the window map (reading B9)
+    GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
+      return launch_roll_accumulate(h->roll, d, slot.lut, slot.data, h->st);
+    }));
   h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
   if (h->pipelined) GVOM_CU(cudaEventRecord(h->ev_integrated, h->st));
@@ -620,13 +674,18 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   if (h->count == 0) return GVOM_E_EMPTY;
   const int newest = (h->head - 1 + h->NS) % h->NS;
   int64_t o[3];
-  for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
+  for (int i = 0; i < 3; ++i) o[i] = h->rolling ? h->origin[i] : h->slots[newest].origin[i];
   if (h->pipelined) GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated, 0));
-  h->map_slots = buffer_slots(h, o);
   h->lp.o_z = o[2];
-  GVOM_CU(stage(
-      h, GVOM_STAGE_COLUMNS, true,
-      [&] { return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->ms()); }, h->ms()));
+  if (h->rolling) {  // the window map at the current origin (reading B9)
+    GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true,
+                  [&] { return launch_columns_roll(h->roll, h->d, h->lp, h->layers, h->st); }));
+  } else {
+    h->map_slots = buffer_slots(h, o);
+    GVOM_CU(stage(
+        h, GVOM_STAGE_COLUMNS, true,
+        [&] { return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->ms()); }, h->ms()));
+  }
   GVOM_CU(surface_layers(h));
   if (h->pipelined)
     GVOM_CU(cudaEventRecord(h->ev_maps[h->maps_calls % gvom_handle::kMapsRing], h->mst));
@@ -849,6 +908,16 @@ gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVOM_LAYER_C
   return GVOM_OK;
 }
 
+gvom_status gvom_export_window(gvom_handle* h, uint64_t* d_hits, uint64_t* d_misses,
+                               uint32_t* d_min_dz, uint64_t* d_m1, uint64_t* d_m2) {
+  if (!h || !d_hits || !d_misses || !d_min_dz || !d_m1 || !d_m2) return GVOM_E_INVALID;
+  if (!h->rolling) return GVOM_E_INVALID;
+  GVOM_CU(stage(h, GVOM_STAGE_EXPORT, true, [&] {
+    return launch_roll_export(h->roll, h->d, d_hits, d_misses, d_min_dz, d_m1, d_m2, h->st);
+  }));
+  return GVOM_OK;
+}
+
 gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]) {
   if (!h || !out_origin) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
@@ -859,6 +928,7 @@ gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]) {
 gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_data, int64_t cap,
                                int64_t* out_k) {
   if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
+  if (h->rolling) return GVOM_E_INVALID;  // see gvom_export_window
   if (!h->maps_valid) return GVOM_E_EMPTY;
   const Dims& d = h->d;
   if (h->mst) GVOM_CU(cudaStreamSynchronize(h->mst));
@@ -904,14 +974,15 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
 
 // ---- multi-GPU slab partition --------------------------------
 static bool slab_ok(const gvom_handle* h, int32_t y0, int32_t y1) {
-  return h && h->cfg.buffer_frames == 1 && !h->pipelined && y0 >= 0 && y1 <= h->cfg.ny && y0 < y1;
+  return h && h->cfg.buffer_frames == 1 && !h->pipelined && !h->rolling && y0 >= 0 &&
+         y1 <= h->cfg.ny && y0 < y1;
 }
 
 gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
                               uint32_t* d_miss, gvom_endpoint* d_ep, int64_t ep_cap,
                               const int32_t* slab_y, int32_t n_ranks, int64_t* out_counts) {
   if (!h || !d_miss || !slab_y || !out_counts || n_ranks < 1 || n_ranks > GVOM_MAX_RANKS ||
-      ep_cap < 0 || (ep_cap > 0 && !d_ep))
+      ep_cap < 0 || (ep_cap > 0 && !d_ep) || h->rolling)
     return GVOM_E_INVALID;
   SlabBounds sb;
   sb.P = n_ranks;

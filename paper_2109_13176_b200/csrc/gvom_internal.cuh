@@ -161,6 +161,27 @@ cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPt
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,
                            const LayerPtrs& out, cudaStream_t st, int64_t cbeg = 0,
                            int64_t cend = -1);
+// ---- rolling map (k_roll.cu; GVOM_FLAG_ROLLING, NEXT-3, reading B9) ----
+struct RollGrid {
+  // per physical voxel P (struct of arrays: a pass-through touches 8 bytes)
+  uint64_t* hits;
+  uint64_t* misses;
+  uint64_t* m1;
+  uint64_t* m2;
+  uint32_t* nmn;   // ~min_dz (0 = no return)
+  uint32_t* bits;  // occupancy (hits >= 1)
+  int64_t ox, oy, oz;  // window origin (world voxels); P = (w mod n) per axis
+  int32_t xo, yo, zo;  // o mod n: logical x -> physical x + xo (wrapped)
+};
+cudaError_t launch_roll_clear(const RollGrid& g, const Dims& d, int axis, int64_t w0, int cnt,
+                              cudaStream_t st);
+cudaError_t launch_roll_accumulate(const RollGrid& g, const Dims& d, const int32_t* lut,
+                                   const gvom_voxel* data, cudaStream_t st);
+cudaError_t launch_columns_roll(const RollGrid& g, const Dims& d, const LayerParams& lp,
+                                const LayerPtrs& out, cudaStream_t st);
+cudaError_t launch_roll_export(const RollGrid& g, const Dims& d, uint64_t* hits, uint64_t* misses,
+                               uint32_t* min_dz, uint64_t* m1, uint64_t* m2, cudaStream_t st);
+
 // ---- multi-GPU slab partition (k_slab.cu) ----
 struct SlabBounds {
   int32_t P;

@@ -93,6 +93,7 @@ def load_library() -> C.CDLL:
         "gvom_export_layers": ([P, P, P], I32),
         "gvom_step": ([P, P, P, I32, P, P, P, P, C.c_size_t, P], I32),
         "gvom_export_layers_cost": ([P, P, P, P, P, C.c_size_t], I32),
+        "gvom_export_window": ([P, P, P, P, P, P], I32),
         "gvom_graph_stats": ([P, P], I32),
         "gvom_map_origin": ([P, P], I32),
         "gvom_export_voxels": ([P, P, P, I64, P], I32),
@@ -124,7 +125,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
-            "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost")
+            "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -135,7 +136,8 @@ def make_config(grid: dict, max_points_per_frame: int) -> Config:
     c.buffer_frames = int(grid.get("buffer_frames", 8))
     c.flags = ((1 if grid.get("pipeline", False) else 0)  # GVOM_FLAG_PIPELINE
                | (2 if grid.get("slope_skip_obstacles", False) else 0)  # ..._SLOPE_SKIP_OBSTACLES
-               | (4 if grid.get("neg_8cone", False) else 0))  # GVOM_FLAG_NEG_8CONE
+               | (4 if grid.get("neg_8cone", False) else 0)  # GVOM_FLAG_NEG_8CONE
+               | (8 if grid.get("rolling", False) else 0))  # GVOM_FLAG_ROLLING
     c.max_points_per_frame = int(max_points_per_frame)
     c.min_obstacle_height = float(grid["min_obstacle_height"])
     c.max_obstacle_height = float(grid["max_obstacle_height"])
@@ -361,6 +363,20 @@ class GvomMap:
             res = {} if res is None else res
             res["cost"] = cost
         return np.array(dlt[:], dtype=np.int64), res
+
+    def export_window(self) -> Dict[str, np.ndarray]:
+        """GVOM_FLAG_ROLLING: the window map, dense in L order (synchronous)."""
+        V = self.nx * self.ny * self.nz
+        t = {k: torch.empty(V, dtype=torch.int64, device=self.device)
+             for k in ("hits", "misses", "m1", "m2")}
+        t["min_dz"] = torch.empty(V, dtype=torch.int32, device=self.device)
+        _check(self.lib.gvom_export_window(self.h, *[C.c_void_p(t[k].data_ptr()) for k in
+                                                      ("hits", "misses", "min_dz", "m1", "m2")]),
+               "gvom_export_window")
+        self.synchronize()
+        out = {k: v.cpu().numpy().view(np.uint64) for k, v in t.items() if k != "min_dz"}
+        out["min_dz"] = t["min_dz"].cpu().numpy().view(np.uint32)
+        return out
 
     def graph_stats(self) -> dict:
         o = (C.c_int64 * 3)()

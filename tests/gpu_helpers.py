@@ -69,6 +69,15 @@ def compare_merged(m: GvomMap, om: "O.OracleMap"):
         assert np.array_equal(data[f], getattr(ref, f)), f"merged {f}"
 
 
+def compare_window(m: GvomMap, om: "O.OracleMap"):
+    """GVOM_FLAG_ROLLING: the window map against the oracle's accumulators."""
+    got = m.export_window()
+    H, Mi, mn, M1, M2 = om.roll
+    for k, ref in (("hits", H), ("misses", Mi), ("min_dz", mn), ("m1", M1), ("m2", M2)):
+        bad = np.flatnonzero(got[k] != ref)
+        assert bad.size == 0, f"window {k} mismatch at {bad.size} voxels, first {bad[:8]}"
+
+
 def layers_np(m: GvomMap) -> dict:
     lay = m.export_layers()
     m.synchronize()  # exports are ordered on the map stream (pipelined mode)
@@ -108,6 +117,8 @@ def run_sequence(w, frames=None, *, host=False, check_every=1, check_merged=True
                 m.synchronize()
                 compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
             compare_layers(layers_np(m), L)
-            if check_merged:
+            if w.grid.get("rolling", False):
+                compare_window(m, om)
+            elif check_merged:
                 compare_merged(m, om)
     return m, om
