@@ -246,8 +246,8 @@ def main_slab(args):
             for i, s in enumerate(f.scans) if i % world == rank]
     npts_all = f.n_points
     stream = torch.cuda.Stream(device=dev)
-    m = GvomMap(grid, max_points_per_frame=max(1, sum(x[0].shape[0] for x in mine)), device=dev,
-                stream=stream)
+    # capacity for the whole frame: data rows sit at their global ranks
+    m = GvomMap(grid, max_points_per_frame=max(1, npts_all), device=dev, stream=stream)
     sm = parallel.SlabMapper(m, ep_capacity=npts_all)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 

@@ -268,16 +268,22 @@ GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_l
 
 /* ---- Multi-GPU slab partition -----------------------------
  * The points of one frame are sharded across P ranks (one process and handle
- * per GPU, buffer_frames must be 1); rank r owns the y-rows
+ * per GPU, not pipelined, not rolling); rank r owns the y-rows
  * [slab_y[r], slab_y[r+1]), which in L order is the contiguous voxel range
  * [slab_y[r]*nx*nz, slab_y[r+1]*nx*nz).  Per frame, with the collectives done
  * by the caller (torch.distributed / NCCL; paper_2109_13176_b200/parallel.py):
  *  1. gvom_partial_scan on the rank's sensors: a dense u32 miss grid [V] and
  *     the in-grid returns as gvom_endpoint records grouped by destination slab;
  *  2. reduce-scatter (SUM) of the miss grids by slab; all-to-all of records;
- *  3. gvom_slab_occupancy -> k of the slab; all-gather of k -> rank base;
- *  4. gvom_slab_finalize: LUT + data rows of the slab (local ranks; global
- *     rank = base + local), pushed into the buffer;
+ *  3. gvom_slab_occupancy -> k of the slab; all-gather of k -> rank base
+ *     (the k of the slabs before it) and the frame's total k;
+ *  4. gvom_slab_finalize(base): LUT + data rows of the slab with GLOBAL ranks
+ *     (data rows at [base, base + k) of the slot, so every rank's
+ *     max_points_per_frame must cover the whole frame), pushed into the buffer;
+ *  4b. with buffer_frames > 1 (motion: the shift of an older map reads rows of
+ *     other slabs): all-gather the slabs' LUT rows and
+ *     data rows into gvom_slot_buffers(age 0) of every rank, then
+ *     gvom_slab_complete(total k): every rank holds the whole frame map;
  *  5. gvom_compute_maps_slab(phase 0): columns of the slab rows; all-gather of
  *     the q_s rows into gvom_surface_buffer(); phase 1: slope, roughness and
  *     negative obstacles for the whole map from the gathered surface.
@@ -295,7 +301,15 @@ GVOM_API gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1,
                                          const gvom_endpoint* d_ep, int64_t n_ep, int64_t* out_k);
 GVOM_API gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
                                         const uint32_t* d_miss_slab, const gvom_endpoint* d_ep,
-                                        int64_t n_ep);
+                                        int64_t n_ep, int64_t base);
+/* Device pointers of buffer map `age` (0 = newest): its LUT [nx*ny*nz] and
+ * data rows [cap] (workspace memory; the caller writes the gathered slabs
+ * into them, ordered on the handle's stream).                             */
+GVOM_API gvom_status gvom_slot_buffers(gvom_handle* h, int32_t age, int32_t** out_d_lut,
+                                       gvom_voxel** out_d_data, int64_t* out_cap);
+/* After the all-gather of step 4b: rebuild the newest map's occupancy from its
+ * complete LUT and set its occupied-voxel count to k_total.               */
+GVOM_API gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total);
 GVOM_API gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1,
                                             int32_t phase);
 /* the stream map processing is enqueued on (the handle's stream unless

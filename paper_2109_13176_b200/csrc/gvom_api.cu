@@ -169,6 +169,7 @@ struct gvom_handle {
   TileCounts tc{};
   // slab partition: occupancy built by gvom_slab_occupancy, pending finalize
   int32_t slab_y0 = -1, slab_y1 = -1;
+  int64_t slab_k = 0;  // occupied voxels of the pending slab
   // fork/join: the cone search runs on `aux` while k_slope runs on `st`
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -974,8 +975,7 @@ gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_lut, gvom_
 
 // ---- multi-GPU slab partition --------------------------------
 static bool slab_ok(const gvom_handle* h, int32_t y0, int32_t y1) {
-  return h && h->cfg.buffer_frames == 1 && !h->pipelined && !h->rolling && y0 >= 0 &&
-         y1 <= h->cfg.ny && y0 < y1;
+  return h && !h->pipelined && !h->rolling && y0 >= 0 && y1 <= h->cfg.ny && y0 < y1;
 }
 
 gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
@@ -1061,15 +1061,17 @@ gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1, const gv
   GVOM_CU(cudaMemcpyAsync(&k, slot.meta, 4, cudaMemcpyDeviceToHost, h->st));
   GVOM_CU(cudaStreamSynchronize(h->st));
   *out_k = k;
+  h->slab_k = k;
   h->slab_y0 = y0;
   h->slab_y1 = y1;
   return GVOM_OK;
 }
 
 gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uint32_t* d_miss_slab,
-                               const gvom_endpoint* d_ep, int64_t n_ep) {
-  if (!slab_ok(h, y0, y1) || !d_miss_slab || n_ep < 0 || (n_ep > 0 && !d_ep))
+                               const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  if (!slab_ok(h, y0, y1) || !d_miss_slab || n_ep < 0 || (n_ep > 0 && !d_ep) || base < 0)
     return GVOM_E_INVALID;
+  if (base + h->slab_k > h->lay.cap) return GVOM_E_SIZE;  // rows [base, base + k)
   if (h->slab_y0 != y0 || h->slab_y1 != y1) return GVOM_E_INVALID;  // occupancy first
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
@@ -1084,7 +1086,7 @@ gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uin
   tc.total = slot.meta;
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
     return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st, t0,
-                                 t1);
+                                 t1, (uint32_t)base);
   }));
   GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
     return launch_endpoint_records((const EpRecord*)d_ep, n_ep, slot.lut, slot.data, h->st);
@@ -1093,6 +1095,27 @@ gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uin
   h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
   h->slab_y0 = h->slab_y1 = -1;
+  return GVOM_OK;
+}
+
+gvom_status gvom_slot_buffers(gvom_handle* h, int32_t age, int32_t** out_d_lut,
+                              gvom_voxel** out_d_data, int64_t* out_cap) {
+  if (!h || !out_d_lut || !out_d_data || !out_cap || age < 0 || age >= h->K) return GVOM_E_INVALID;
+  const int idx = ((h->head - 1 - age) % h->NS + h->NS) % h->NS;
+  *out_d_lut = h->slots[idx].lut;
+  *out_d_data = h->slots[idx].data;
+  *out_cap = h->lay.cap;
+  return GVOM_OK;
+}
+
+gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total) {
+  if (!h || h->pipelined || h->rolling || h->count == 0 || k_total < 0 || k_total > h->lay.cap)
+    return GVOM_E_INVALID;
+  Slot& slot = h->slots[(h->head - 1 + h->NS) % h->NS];
+  GVOM_CU(stage(h, GVOM_STAGE_RANK_COUNT, true, [&] {
+    return launch_bits_from_lut(slot.lut, slot.bits, slot.wprefix, h->d, slot.meta,
+                                (uint32_t)k_total, h->st);
+  }));
   return GVOM_OK;
 }
 

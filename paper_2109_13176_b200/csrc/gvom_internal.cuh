@@ -145,9 +145,11 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
                            uint32_t* bits, const TileCounts& tc, bool last_launch,
                            cudaStream_t st);
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
+// base: added to every rank (a slab's global rank offset, 0 otherwise)
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
-                                  cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1);
+                                  cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1,
+                                  uint32_t base = 0);
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st);
@@ -201,6 +203,10 @@ cudaError_t launch_tile_scan(const TileCounts& tc, int64_t t_begin, int64_t t_en
                              cudaStream_t st);
 cudaError_t launch_endpoint_records(const EpRecord* ep, int64_t n, const int32_t* lut,
                                     gvom_voxel* data, cudaStream_t st);
+// occupancy bits and per-word rank prefix of a whole slot rebuilt from its
+// LUT (after the slabs' LUT rows were all-gathered); *meta = k_total
+cudaError_t launch_bits_from_lut(const int32_t* lut, uint32_t* bits, uint32_t* wprefix,
+                                 const Dims& d, uint32_t* meta, uint32_t k_total, cudaStream_t st);
 cudaError_t launch_transpose_init(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                                   cudaStream_t st);
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,

@@ -552,11 +552,12 @@ __global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na
 // voxels with 16-byte accesses.
 __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
-    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t_begin) {
+    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t_begin,
+    uint32_t base) {
   __shared__ uint32_t sbits[kTileWords], spre[kTileWords], wsum[kTileWords / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t b = t_begin + blockIdx.x;
-  const uint32_t off = __ldg(tc.offset + b);  // rank offset of this tile
+  const uint32_t off = base + __ldg(tc.offset + b);  // rank offset of this tile
   // per-word exclusive prefix within the tile
   const int64_t w = b * kTileWords + t;
   const uint32_t bw = w < d.W ? __ldg(bits + w) : 0u;
@@ -745,11 +746,11 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
 
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
-                                  cudaStream_t st, int64_t t_begin, int64_t t_end) {
+                                  cudaStream_t st, int64_t t_begin, int64_t t_end, uint32_t base) {
   if (t_end < 0) t_end = n_tiles(d);
   if (t_end <= t_begin) return cudaSuccess;
   k_finalize_tiles<<<(unsigned)(t_end - t_begin), kTileWords, 0, st>>>(lut_inplace, bits, wprefix,
-                                                                       data, tc, d, t_begin);
+                                                                       data, tc, d, t_begin, base);
   return cudaGetLastError();
 }
 

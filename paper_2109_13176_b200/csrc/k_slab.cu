@@ -177,6 +177,30 @@ __global__ void __launch_bounds__(256) k_transpose_init(const Dims d, const Laye
   out.nmax[c] = INT32_MIN;
 }
 
+// occupancy word w and its rank prefix (the rank of its first occupied voxel;
+// only read for words with a set bit) from a complete LUT
+__global__ void __launch_bounds__(256) k_bits_from_lut(const int32_t* __restrict__ lut,
+                                                       uint32_t* __restrict__ bits,
+                                                       uint32_t* __restrict__ wprefix,
+                                                       const Dims d, uint32_t* meta,
+                                                       uint32_t k_total) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w == 0) *meta = k_total;
+  if (w >= d.W) return;
+  uint32_t m = 0, first = 0;
+  const int64_t L0 = w * 32;
+  for (int i = 31; i >= 0; --i) {
+    if (L0 + i >= d.V) continue;
+    const int32_t v = __ldg(lut + L0 + i);
+    if (v >= 0) {
+      m |= 1u << i;
+      first = (uint32_t)v;
+    }
+  }
+  bits[w] = m;
+  wprefix[w] = first;
+}
+
 inline unsigned blocks_for(int64_t n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
 
 }  // namespace
@@ -213,6 +237,12 @@ cudaError_t launch_endpoint_records(const EpRecord* ep, int64_t n, const int32_t
                                     gvom_voxel* data, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_endpoint_records<<<blocks_for(n, 256), 256, 0, st>>>(ep, n, lut, data);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bits_from_lut(const int32_t* lut, uint32_t* bits, uint32_t* wprefix,
+                                 const Dims& d, uint32_t* meta, uint32_t k_total, cudaStream_t st) {
+  k_bits_from_lut<<<blocks_for(d.W, 256), 256, 0, st>>>(lut, bits, wprefix, d, meta, k_total);
   return cudaGetLastError();
 }
 

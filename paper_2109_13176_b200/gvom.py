@@ -104,7 +104,9 @@ def load_library() -> C.CDLL:
         "gvom_status_string": ([I32], C.c_char_p),
         "gvom_partial_scan": ([P, P, I32, P, P, I64, P, I32, P], I32),
         "gvom_slab_occupancy": ([P, I32, I32, P, I64, P], I32),
-        "gvom_slab_finalize": ([P, I32, I32, P, P, I64], I32),
+        "gvom_slab_finalize": ([P, I32, I32, P, P, I64, I64], I32),
+        "gvom_slot_buffers": ([P, I32, P, P, P], I32),
+        "gvom_slab_complete": ([P, I64], I32),
         "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
         "gvom_surface_buffer": ([P, P], I32),
         "gvom_map_stream": ([P, P], I32),
@@ -125,7 +127,8 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_set_timing", "gvom_stage_times", "gvom_launch_count", "gvom_status_string",
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
-            "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window")
+            "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
+            "gvom_slot_buffers", "gvom_slab_complete")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -259,10 +262,32 @@ class GvomMap:
         return k.value
 
     def slab_finalize(self, y0: int, y1: int, miss_slab: torch.Tensor, records: torch.Tensor,
-                      n: int):
+                      n: int, base: int = 0):
+        """LUT + data rows of the slab with global ranks (rows [base, base + k))."""
         _check(self.lib.gvom_slab_finalize(self.h, y0, y1, C.c_void_p(miss_slab.data_ptr()),
-                                           C.c_void_p(records.data_ptr()), n),
+                                           C.c_void_p(records.data_ptr()), n, int(base)),
                "gvom_slab_finalize")
+
+    def slot_buffers(self, age: int = 0):
+        """(LUT int32 [V], data rows int64 [cap, 4]) of buffer map `age`, as
+        torch views of the workspace (no copy; for the slab all-gather)."""
+        lp, dp, cap = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _check(self.lib.gvom_slot_buffers(self.h, int(age), C.byref(lp), C.byref(dp),
+                                          C.byref(cap)), "gvom_slot_buffers")
+        V = self.nx * self.ny * self.nz
+
+        class _View:  # __cuda_array_interface__ wrapper of library-owned memory
+            def __init__(self, ptr, shape, typestr):
+                self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr,
+                                                 "data": (ptr, False), "version": 3,
+                                                 "strides": None}
+        lut = torch.as_tensor(_View(lp.value, (V,), "<i4"), device=self.device)
+        data = torch.as_tensor(_View(dp.value, (max(int(cap.value), 1), 4), "<i8"),
+                               device=self.device)
+        return lut, data
+
+    def slab_complete(self, k_total: int):
+        _check(self.lib.gvom_slab_complete(self.h, int(k_total)), "gvom_slab_complete")
 
     def compute_maps_slab(self, y0: int, y1: int, phase: int):
         _check(self.lib.gvom_compute_maps_slab(self.h, y0, y1, phase), "gvom_compute_maps_slab")

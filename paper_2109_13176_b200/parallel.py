@@ -9,6 +9,9 @@ tests).  Rank r of P owns the y-rows [y_r, y_{r+1}) of the map; in L order
   returns      -> all_to_all_single of 8-byte (L, dz) records to the slab owner
   slab k       -> all_gather: global rank of a slab's voxel = sum of the k of the
                   slabs before it + its local rank (ranks stay in L order)
+  frame map    -> (buffer_frames > 1, motion; NEXT-2) all_gather of the LUT
+                  slabs + one broadcast of data rows per rank: every rank holds
+                  every buffered frame whole, so shifted maps read any row
   surface rows -> all_gather_into_tensor of q_s rows (slope / cone-search halos)
 
 The compute steps are the C-ABI slab calls (gvom_partial_scan,
@@ -66,6 +69,21 @@ def rank_base(k_local: int, device, group=None) -> Tuple[int, int, List[int]]:
     return sum(ks[:r]), sum(ks), ks
 
 
+def gather_frame(lut: torch.Tensor, data: torch.Tensor, rows: int, y0: int, y1: int,
+                 bases: Sequence[int], ks: Sequence[int], group=None):
+    """NEXT-2 (K > 1, motion): make a slab-finalized frame map whole on every
+    rank.  lut: int32 [V] with this rank's slab rows [y0, y1) valid (global
+    ranks); data: rows [cap, 4] int64 with this rank's rows at [base, base+k).
+    All-gather of the equal LUT slabs, then one broadcast per rank of its
+    data rows (their counts differ)."""
+    P = dist.get_world_size(group)
+    mine = lut[y0 * rows:y1 * rows].clone()
+    dist.all_gather_into_tensor(lut[:P * mine.numel()], mine, group=group)
+    for r in range(P):
+        if ks[r] > 0:
+            dist.broadcast(data[bases[r]:bases[r] + ks[r]], src=r, group=group)
+
+
 def gather_rows(full: torch.Tensor, y0: int, y1: int, group=None):
     """all-gather equal row slabs of a [ny, ...] tensor in place."""
     mine = full[y0:y1].contiguous().clone()
@@ -73,7 +91,9 @@ def gather_rows(full: torch.Tensor, y0: int, y1: int, group=None):
 
 
 class SlabMapper:
-    """Drives one rank's GvomMap (buffer_frames = 1) through a distributed frame."""
+    """Drives one rank's GvomMap through a distributed frame.  With
+    buffer_frames > 1 every finalized frame map is made whole on every rank
+    (gather_frame) so that the shift of older maps can read any row."""
 
     def __init__(self, m, group=None, ep_capacity: Optional[int] = None):
         self.m = m
@@ -95,8 +115,16 @@ class SlabMapper:
         miss_slab = exchange_misses(self.miss, self.group)
         recv = route_records(self.records, counts, self.group)
         k = self.m.slab_occupancy(self.y0, self.y1, recv, recv.numel())
-        self.base, self.k_total, _ = rank_base(k, self.m.device, self.group)
-        self.m.slab_finalize(self.y0, self.y1, miss_slab, recv, recv.numel())
+        self.base, self.k_total, ks = rank_base(k, self.m.device, self.group)
+        self.m.slab_finalize(self.y0, self.y1, miss_slab, recv, recv.numel(), self.base)
+        if int(self.m.cfg.buffer_frames) > 1:
+            lut, data = self.m.slot_buffers(0)
+            bases = [sum(ks[:r]) for r in range(self.P)]
+            torch.cuda.current_stream(self.m.device).wait_stream(self.m.stream)
+            gather_frame(lut, data, self.m.nx * self.m.nz, self.y0, self.y1, bases, ks,
+                         self.group)
+            self.m.stream.wait_stream(torch.cuda.current_stream(self.m.device))
+            self.m.slab_complete(self.k_total)
 
     def compute_maps(self):
         self.m.compute_maps_slab(self.y0, self.y1, 0)

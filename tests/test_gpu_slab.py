@@ -8,6 +8,8 @@ height / density / hard / soft of the slab rows, and slope / roughness /
 negative obstacles of the whole map.  (No rank waits on another inside a
 kernel, so this emulation is faithful.)
 """
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -59,7 +61,7 @@ def _run(w, P):
     for r in range(P):
         m = ranks[r][0]
         miss_slab, recv = states[r]
-        m.slab_finalize(ys[r], ys[r + 1], miss_slab, recv, recv.numel())
+        m.slab_finalize(ys[r], ys[r + 1], miss_slab, recv, recv.numel(), int(bases[r]))
         m.compute_maps_slab(ys[r], ys[r + 1], 0)
     # emulated all-gather of the surface rows
     surf = torch.cat([ranks[r][0].surface()[ys[r]:ys[r + 1]] for r in range(P)])
@@ -72,11 +74,11 @@ def _run(w, P):
         m = ranks[r][0]
         lut, data, _ = m.export_frame(0)
         v0, v1 = ys[r] * row, ys[r + 1] * row
-        got = lut[v0:v1].astype(np.int64)
-        got = np.where(got >= 0, got + bases[r], got)
-        assert np.array_equal(got, ref_lut[v0:v1].astype(np.int64)), f"rank {r} LUT"
+        # global ranks: the slab's LUT rows and its data rows [base, base + k)
+        assert np.array_equal(lut[v0:v1], ref_lut[v0:v1]), f"rank {r} LUT"
         for k_ in ("hits", "misses", "min_dz", "m1", "m2"):
-            assert np.array_equal(data[k_], ref_data[k_][bases[r]:bases[r + 1]]), (r, k_)
+            assert np.array_equal(data[k_][bases[r]:bases[r + 1]],
+                                  ref_data[k_][bases[r]:bases[r + 1]]), (r, k_)
         lay = layers_np(m)
         sl = slice(ys[r], ys[r + 1])
         for k_ in ("height", "density", "hard", "soft"):
@@ -99,3 +101,104 @@ def test_slab_partition_c1_eight_ranks():
 @pytest.mark.slow
 def test_slab_partition_c5_eight_ranks():
     _run(synth.workload(4), 8)
+
+
+def _run_sequence(w, P, K, frames):
+    """NEXT-2: motion with a K-map buffer.  Every frame: the slab steps on P
+    emulated ranks, the frame-map gather (LUT slabs + data rows into every
+    rank's newest slot, then gvom_slab_complete), the slab column pass and the
+    surface gather; compared with one GPU after every frame."""
+    grid = dict(w.grid)
+    grid["buffer_frames"] = K
+    npts = max(f.n_points for f in frames)
+    ref = GvomMap(grid, max_points_per_frame=npts)
+    ms = [GvomMap(grid, max_points_per_frame=npts) for _ in range(P)]
+    nx, ny, nz = ref.nx, ref.ny, ref.nz
+    ys = parallel.slab_rows(ny, P)
+    row = nx * nz
+    V = nx * ny * nz
+    for f in frames:
+        scans = [(torch.from_numpy(s.points).cuda(), s.pose, s.rings) for s in f.scans]
+        ref.shift(f.vehicle_xyz)
+        ref.integrate_scan(scans)
+        ref.compute_maps()
+        ref_layers = layers_np(ref)
+        st = []
+        for r, m in enumerate(ms):
+            m.shift(f.vehicle_xyz)
+            miss = torch.empty(V, dtype=torch.int32, device="cuda")
+            rec = torch.empty(npts + 1, dtype=torch.int64, device="cuda")
+            mine = [s for i, s in enumerate(scans) if i % P == r]
+            st.append((miss, rec, m.partial_scan(mine, miss, rec, ys)))
+        total_miss = sum(x[0] for x in st)
+        offs = [np.concatenate([[0], np.cumsum(x[2])]) for x in st]
+        recvs, ks = [], []
+        for r, m in enumerate(ms):
+            recv = torch.cat([x[1][int(o[r]):int(o[r + 1])] for x, o in zip(st, offs)]).contiguous()
+            ks.append(m.slab_occupancy(ys[r], ys[r + 1], recv, recv.numel()))
+            recvs.append(recv)
+        bases = np.concatenate([[0], np.cumsum(ks)])
+        for r, m in enumerate(ms):
+            miss_slab = total_miss[ys[r] * row:ys[r + 1] * row].contiguous()
+            m.slab_finalize(ys[r], ys[r + 1], miss_slab, recvs[r], recvs[r].numel(),
+                            int(bases[r]))
+        torch.cuda.synchronize()
+        # emulated gather_frame: every rank's newest slot gets every slab
+        bufs = [m.slot_buffers(0) for m in ms]
+        for r in range(P):
+            for q in range(P):
+                if q == r:
+                    continue
+                bufs[r][0][ys[q] * row:ys[q + 1] * row] = bufs[q][0][ys[q] * row:ys[q + 1] * row]
+                bufs[r][1][int(bases[q]):int(bases[q + 1])] = \
+                    bufs[q][1][int(bases[q]):int(bases[q + 1])]
+        torch.cuda.synchronize()
+        for m in ms:
+            m.slab_complete(int(bases[-1]))
+        ref_lut, ref_data, _ = ref.export_frame(0)
+        for r, m in enumerate(ms):
+            lut, data, _ = m.export_frame(0)
+            assert np.array_equal(lut, ref_lut), f"rank {r} frame LUT"
+            for k_ in ("hits", "misses", "min_dz", "m1", "m2"):
+                assert np.array_equal(data[k_], ref_data[k_]), (r, k_)
+            m.compute_maps_slab(ys[r], ys[r + 1], 0)
+        surf = torch.cat([ms[r].surface()[ys[r]:ys[r + 1]] for r in range(P)])
+        for r, m in enumerate(ms):
+            m.surface().copy_(surf)
+            m.compute_maps_slab(ys[r], ys[r + 1], 1)
+        torch.cuda.synchronize()
+        for r, m in enumerate(ms):
+            lay = layers_np(m)
+            sl = slice(ys[r], ys[r + 1])
+            for k_ in ("height", "density", "hard", "soft"):
+                a, b = lay[k_][sl], ref_layers[k_][sl]
+                assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
+            for k_ in ("slope", "roughness", "neg"):
+                a, b = lay[k_], ref_layers[k_]
+                assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_partition_with_motion_k8(P):
+    # BASELINE configs[2] (c3, OS1-128, 12 m/s): shift + merge of 8 maps, slabbed
+    w = synth.config3(speed=12.0, n_frames=10, columns=512)
+    _run_sequence(w, P, 8, w.frames)
+
+
+def test_slab_partition_with_motion_multi_sensor():
+    # c4's three lidars over a moving sequence (sensors dealt round-robin), K = 3
+    w = synth.workload(3)
+    f0 = w.frames[0]
+    frames = []
+    for i in range(4):
+        dx = 0.7 * i
+        scans = [dataclasses.replace(s, pose=_moved(s.pose, dx)) for s in f0.scans]
+        x, y, z = f0.vehicle_xyz
+        frames.append(dataclasses.replace(f0, vehicle_xyz=(x + dx, y, z), scans=scans))
+    _run_sequence(w, 2, 3, frames)
+
+
+def _moved(pose, dx):
+    p = np.array(pose, dtype=np.float64).reshape(3, 4).copy()
+    p[0, 3] += dx
+    return p

@@ -105,6 +105,24 @@ def _worker(rank, world, port, q):
         assert np.array_equal(lut_got, lut_ref)
         for f in ("hits", "misses", "min_dz", "m1", "m2"):
             assert np.array_equal(getattr(fm, f), getattr(ref, f)[base:base + fm.k]), f
+        # --- NEXT-2 frame gather (K > 1): every rank ends with the whole map -
+        def rows_of(x, lo, n):  # gvom_voxel rows as int64 words [n, 4]
+            w = np.zeros((n, 4), np.uint64)
+            w[:, 0] = x.hits[lo:lo + n].astype(np.uint64) | (
+                x.misses[lo:lo + n].astype(np.uint64) << np.uint64(32))
+            w[:, 1] = x.min_dz[lo:lo + n].astype(np.uint64)
+            w[:, 2] = x.m1[lo:lo + n]
+            w[:, 3] = x.m2[lo:lo + n]
+            return w.view(np.int64)
+        lut_full = torch.full((V,), -7, dtype=torch.int32)
+        lut_full[v0:v1] = torch.from_numpy(np.where(fm.lut >= 0, fm.lut + base, fm.lut)
+                                           .astype(np.int32))
+        data = torch.full((k_total + 3, 4), -9, dtype=torch.int64)
+        data[base:base + fm.k] = torch.from_numpy(rows_of(fm, 0, fm.k))
+        bases = [sum(ks[:r]) for r in range(world)]
+        parallel.gather_frame(lut_full, data, nx * nz, y0, y1, bases, ks)
+        assert np.array_equal(lut_full.numpy(), ref.lut)
+        assert np.array_equal(data[:k_total].numpy(), rows_of(ref, 0, ref.k))
         # --- surface rows: columns of the slab, then all-gather ------------
         T = O.thresholds(res, grid["min_obstacle_height"], grid["max_obstacle_height"],
                          grid["density_threshold"], grid["neg_obs_threshold"])
