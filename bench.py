@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--neg8cone", action="store_true",
                     help="GVOM_FLAG_NEG_8CONE variant (8-cone negative-obstacle search)")
+    ap.add_argument("--fused", action="store_true",
+                    help="slab path: miss grids in symmetric memory, summed by the slab "
+                         "finalize over peer memory (gvom_slab_finalize_peers)")
     ap.add_argument("--rolling", action="store_true",
                     help="GVOM_FLAG_ROLLING variant (one accumulated window map, K = inf)")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
@@ -248,7 +251,7 @@ def main_slab(args):
     stream = torch.cuda.Stream(device=dev)
     # capacity for the whole frame: data rows sit at their global ranks
     m = GvomMap(grid, max_points_per_frame=max(1, npts_all), device=dev, stream=stream)
-    sm = parallel.SlabMapper(m, ep_capacity=npts_all)
+    sm = parallel.SlabMapper(m, ep_capacity=npts_all, fused=args.fused)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step():
@@ -283,7 +286,9 @@ def main_slab(args):
             "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
             "config": {"workload": w.name, "points_per_frame": npts_all, "sensors": len(f.scans),
                        "grid": f"{m.nx}x{m.ny}x{m.nz}@{w.grid['res']}m", "buffer_frames": 1,
-                       "parallelism": f"slab{world}: sensors sharded, reduce-scatter by y-slab",
+                       "parallelism": f"slab{world}: sensors sharded, " + (
+                           "miss grids summed over peer memory in the slab finalize"
+                           if args.fused else "reduce-scatter by y-slab"),
                        "l2": "flushed (256 MiB write) between steps",
                        "step": "shift+partial_scan+exchange+slab_finalize+slab maps"},
             "map_updates_per_s": args.steps / (total / 1e3),

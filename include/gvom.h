@@ -302,6 +302,18 @@ GVOM_API gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1,
 GVOM_API gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
                                         const uint32_t* d_miss_slab, const gvom_endpoint* d_ep,
                                         int64_t n_ep, int64_t base);
+/* NEXT-2 fused collective: steps 2 (the reduce-scatter of miss grids) and 4
+ * in one kernel.  d_miss_grids: host array of the P ranks' partial miss grids
+ * [V] (u32, 16-byte aligned) as device pointers this GPU can load from --
+ * peer memory (e.g. torch symmetric memory buffer_ptrs, after a barrier that
+ * orders the ranks' gvom_partial_scan before it); the finalize sums them over
+ * the slab's tiles as it encodes them.  Same result as gvom_slab_finalize on
+ * the reduce-scattered slab.  The grids must stay unchanged until the
+ * handle's stream has passed this call.                                   */
+GVOM_API gvom_status gvom_slab_finalize_peers(gvom_handle* h, int32_t y0, int32_t y1,
+                                              const uint32_t* const* d_miss_grids,
+                                              int32_t n_grids, const gvom_endpoint* d_ep,
+                                              int64_t n_ep, int64_t base);
 /* Device pointers of buffer map `age` (0 = newest): its LUT [nx*ny*nz] and
  * data rows [cap] (workspace memory; the caller writes the gathered slabs
  * into them, ordered on the handle's stream).                             */

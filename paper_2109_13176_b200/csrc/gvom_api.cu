@@ -1067,26 +1067,30 @@ gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1, const gv
   return GVOM_OK;
 }
 
-gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uint32_t* d_miss_slab,
-                               const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
-  if (!slab_ok(h, y0, y1) || !d_miss_slab || n_ep < 0 || (n_ep > 0 && !d_ep) || base < 0)
-    return GVOM_E_INVALID;
-  if (base + h->slab_k > h->lay.cap) return GVOM_E_SIZE;  // rows [base, base + k)
+// Slab finalize: the slab's miss counts come either from the reduce-scattered
+// slab rows (d_miss_slab, copied into the slot) or, fused, from the P ranks'
+// partial grids read over peer memory by the finalize itself (peers).
+static gvom_status slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
+                                 const uint32_t* d_miss_slab, const PeerGrids* peers,
+                                 const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  if (!slab_ok(h, y0, y1) || n_ep < 0 || (n_ep > 0 && !d_ep) || base < 0) return GVOM_E_INVALID;
   if (h->slab_y0 != y0 || h->slab_y1 != y1) return GVOM_E_INVALID;  // occupancy first
+  if (base + h->slab_k > h->lay.cap) return GVOM_E_SIZE;  // rows [base, base + k)
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
   const int64_t row = (int64_t)h->cfg.nx * h->cfg.nz;
-  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
-    return cudaMemcpyAsync(slot.lut + y0 * row, d_miss_slab, 4 * (size_t)((y1 - y0) * row),
-                           cudaMemcpyDeviceToDevice, h->st);
-  }));
+  if (!peers)
+    GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+      return cudaMemcpyAsync(slot.lut + y0 * row, d_miss_slab, 4 * (size_t)((y1 - y0) * row),
+                             cudaMemcpyDeviceToDevice, h->st);
+    }));
   int64_t t0, t1;
   slab_tiles(h, y0, y1, &t0, &t1);
   TileCounts tc = h->tc;
   tc.total = slot.meta;
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
     return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st, t0,
-                                 t1, (uint32_t)base);
+                                 t1, (uint32_t)base, peers);
   }));
   GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
     return launch_endpoint_records((const EpRecord*)d_ep, n_ep, slot.lut, slot.data, h->st);
@@ -1096,6 +1100,25 @@ gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uin
   if (h->count < h->K) h->count++;
   h->slab_y0 = h->slab_y1 = -1;
   return GVOM_OK;
+}
+
+gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uint32_t* d_miss_slab,
+                               const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  if (!d_miss_slab) return GVOM_E_INVALID;
+  return slab_finalize(h, y0, y1, d_miss_slab, nullptr, d_ep, n_ep, base);
+}
+
+gvom_status gvom_slab_finalize_peers(gvom_handle* h, int32_t y0, int32_t y1,
+                                     const uint32_t* const* d_miss_grids, int32_t n_grids,
+                                     const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  if (!d_miss_grids || n_grids < 1 || n_grids > GVOM_MAX_RANKS) return GVOM_E_INVALID;
+  PeerGrids pg{};
+  pg.P = n_grids;
+  for (int p = 0; p < n_grids; ++p) {
+    if (!d_miss_grids[p] || ((uintptr_t)d_miss_grids[p] & 15) != 0) return GVOM_E_INVALID;
+    pg.g[p] = d_miss_grids[p];
+  }
+  return slab_finalize(h, y0, y1, nullptr, &pg, d_ep, n_ep, base);
 }
 
 gvom_status gvom_slot_buffers(gvom_handle* h, int32_t age, int32_t** out_d_lut,

@@ -145,11 +145,17 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
                            uint32_t* bits, const TileCounts& tc, bool last_launch,
                            cudaStream_t st);
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
+// the P ranks' partial miss grids, device pointers the GPU can load from
+// (peer memory, NEXT-2): the finalize sums them instead of reading lut_inplace
+struct PeerGrids {
+  const uint32_t* g[GVOM_MAX_RANKS];
+  int32_t P;
+};
 // base: added to every rank (a slab's global rank offset, 0 otherwise)
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
                                   cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1,
-                                  uint32_t base = 0);
+                                  uint32_t base = 0, const PeerGrids* peers = nullptr);
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st);

@@ -550,10 +550,37 @@ __global__ void __launch_bounds__(256) k_zero3(uint4* __restrict__ a, int64_t na
 // block, so no block waits on another.  Then: per-word prefix (block scan),
 // wprefix store, and the in-place LUT encode / data-row init of its 8192
 // voxels with 16-byte accesses.
+// kPeers (NEXT-2, fused collective): the miss count of voxel L is the sum of
+// the P ranks' partial grids peers.g[p][L], read over peer memory as the tile
+// is encoded -- the reduce-scatter of the grids fused into the finalize.
+template <bool kPeers>
+__device__ __forceinline__ uint4 miss4(const int32_t* __restrict__ buf, const PeerGrids& peers,
+                                       int64_t L) {
+  if (!kPeers) return __ldcs(reinterpret_cast<const uint4*>(buf + L));
+  uint4 s = make_uint4(0u, 0u, 0u, 0u);
+  for (int p = 0; p < peers.P; ++p) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(peers.g[p] + L));
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+    s.w += v.w;
+  }
+  return s;
+}
+template <bool kPeers>
+__device__ __forceinline__ uint32_t miss1(const int32_t* __restrict__ buf, const PeerGrids& peers,
+                                          int64_t L) {
+  if (!kPeers) return (uint32_t)buf[L];
+  uint32_t s = 0;
+  for (int p = 0; p < peers.P; ++p) s += __ldcs(peers.g[p] + L);
+  return s;
+}
+
+template <bool kPeers>
 __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     int32_t* __restrict__ buf, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
     gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t_begin,
-    uint32_t base) {
+    uint32_t base, const __grid_constant__ PeerGrids peers) {
   __shared__ uint32_t sbits[kTileWords], spre[kTileWords], wsum[kTileWords / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int64_t b = t_begin + blockIdx.x;
@@ -585,7 +612,7 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     uint4 mv[kIt];
 #pragma unroll
     for (int it = 0; it < kIt; ++it)
-      mv[it] = __ldcs(reinterpret_cast<const uint4*>(buf + vbase + t * 4 + it * kTileWords * 4));
+      mv[it] = miss4<kPeers>(buf, peers, vbase + t * 4 + it * kTileWords * 4);
 #pragma unroll
     for (int it = 0; it < kIt; ++it) {
       const int i = t * 4 + it * kTileWords * 4;
@@ -614,7 +641,7 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
     if (L >= d.V) break;
     const uint32_t ww = sbits[i >> 5], pp = spre[i >> 5];
     uint32_t m[4];
-    for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? (uint32_t)buf[L + j] : 0u;
+    for (int j = 0; j < 4; ++j) m[j] = (L + j < d.V) ? miss1<kPeers>(buf, peers, L + j) : 0u;
     for (int j = 0; j < 4; ++j) {
       if (L + j >= d.V) break;
       const int bit = (i + j) & 31;
@@ -746,11 +773,19 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
 
 cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, uint32_t* wprefix,
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
-                                  cudaStream_t st, int64_t t_begin, int64_t t_end, uint32_t base) {
+                                  cudaStream_t st, int64_t t_begin, int64_t t_end, uint32_t base,
+                                  const PeerGrids* peers) {
   if (t_end < 0) t_end = n_tiles(d);
   if (t_end <= t_begin) return cudaSuccess;
-  k_finalize_tiles<<<(unsigned)(t_end - t_begin), kTileWords, 0, st>>>(lut_inplace, bits, wprefix,
-                                                                       data, tc, d, t_begin, base);
+  const unsigned grid = (unsigned)(t_end - t_begin);
+  if (peers && peers->P > 0) {
+    k_finalize_tiles<true><<<grid, kTileWords, 0, st>>>(lut_inplace, bits, wprefix, data, tc, d,
+                                                       t_begin, base, *peers);
+  } else {
+    PeerGrids none{};
+    k_finalize_tiles<false><<<grid, kTileWords, 0, st>>>(lut_inplace, bits, wprefix, data, tc, d,
+                                                        t_begin, base, none);
+  }
   return cudaGetLastError();
 }
 

@@ -106,6 +106,7 @@ def load_library() -> C.CDLL:
         "gvom_slab_occupancy": ([P, I32, I32, P, I64, P], I32),
         "gvom_slab_finalize": ([P, I32, I32, P, P, I64, I64], I32),
         "gvom_slot_buffers": ([P, I32, P, P, P], I32),
+        "gvom_slab_finalize_peers": ([P, I32, I32, P, I32, P, I64, I64], I32),
         "gvom_slab_complete": ([P, I64], I32),
         "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
         "gvom_surface_buffer": ([P, P], I32),
@@ -128,7 +129,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
-            "gvom_slot_buffers", "gvom_slab_complete")
+            "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -267,6 +268,16 @@ class GvomMap:
         _check(self.lib.gvom_slab_finalize(self.h, y0, y1, C.c_void_p(miss_slab.data_ptr()),
                                            C.c_void_p(records.data_ptr()), n, int(base)),
                "gvom_slab_finalize")
+
+    def slab_finalize_peers(self, y0: int, y1: int, grid_ptrs, records: torch.Tensor, n: int,
+                            base: int = 0):
+        """Fused reduce-scatter + finalize: grid_ptrs are the P ranks' partial
+        miss grids (device pointers this GPU can load from, e.g. symmetric
+        memory buffer_ptrs)."""
+        arr = (C.c_void_p * len(grid_ptrs))(*[int(p) for p in grid_ptrs])
+        _check(self.lib.gvom_slab_finalize_peers(self.h, y0, y1, arr, len(grid_ptrs),
+                                                 C.c_void_p(records.data_ptr()), n, int(base)),
+               "gvom_slab_finalize_peers")
 
     def slot_buffers(self, age: int = 0):
         """(LUT int32 [V], data rows int64 [cap, 4]) of buffer map `age`, as

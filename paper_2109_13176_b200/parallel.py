@@ -5,7 +5,9 @@ tests).  Rank r of P owns the y-rows [y_r, y_{r+1}) of the map; in L order
 (z + nz*(x + nx*y)) that is one contiguous voxel range, so the exchange is:
 
   miss grids   -> reduce_scatter_tensor(SUM): integer sums, exact  ("hits
-                  and misses being added together")
+                  and misses being added together"); or, fused (NEXT-2), the
+                  grids in symmetric memory and the slab finalize summing every
+                  rank's grid over peer memory (gvom_slab_finalize_peers)
   returns      -> all_to_all_single of 8-byte (L, dz) records to the slab owner
   slab k       -> all_gather: global rank of a slab's voxel = sum of the k of the
                   slabs before it + its local rank (ranks stay in L order)
@@ -95,7 +97,7 @@ class SlabMapper:
     buffer_frames > 1 every finalized frame map is made whole on every rank
     (gather_frame) so that the shift of older maps can read any row."""
 
-    def __init__(self, m, group=None, ep_capacity: Optional[int] = None):
+    def __init__(self, m, group=None, ep_capacity: Optional[int] = None, fused: bool = False):
         self.m = m
         self.group = group
         self.P = dist.get_world_size(group)
@@ -104,19 +106,44 @@ class SlabMapper:
         self.y0, self.y1 = self.ys[self.rank], self.ys[self.rank + 1]
         V = m.nx * m.ny * m.nz
         dev = m.device
-        self.miss = torch.empty(V, dtype=torch.int32, device=dev)
+        # fused (NEXT-2): the miss grids live in symmetric memory and the slab
+        # finalize reads every rank's grid over peer memory
+        # (gvom_slab_finalize_peers) instead of a reduce-scatter
+        self.fused = fused
+        if fused:
+            import torch.distributed._symmetric_memory as symm_mem
+            self.miss = symm_mem.empty(V, dtype=torch.int32, device=dev)
+            grp = group if group is not None else dist.group.WORLD
+            self.symm = symm_mem.rendezvous(self.miss, grp.group_name)
+            self.grid_ptrs = list(self.symm.buffer_ptrs)
+        else:
+            self.miss = torch.empty(V, dtype=torch.int32, device=dev)
         cap = ep_capacity or int(m.cfg.max_points_per_frame)
         self.records = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
         self.base = 0
         self.k_total = 0
 
     def integrate(self, scans_local):
+        cur = torch.cuda.current_stream(self.m.device)
+        if self.fused:  # no rank still reads our grid of the previous frame
+            cur.wait_stream(self.m.stream)
+            self.symm.barrier()
+            self.m.stream.wait_stream(cur)
         counts = self.m.partial_scan(scans_local, self.miss, self.records, self.ys)
-        miss_slab = exchange_misses(self.miss, self.group)
+        if self.fused:  # every rank's grid of this frame is complete
+            cur.wait_stream(self.m.stream)
+            self.symm.barrier()
+            self.m.stream.wait_stream(cur)
+        else:
+            miss_slab = exchange_misses(self.miss, self.group)
         recv = route_records(self.records, counts, self.group)
         k = self.m.slab_occupancy(self.y0, self.y1, recv, recv.numel())
         self.base, self.k_total, ks = rank_base(k, self.m.device, self.group)
-        self.m.slab_finalize(self.y0, self.y1, miss_slab, recv, recv.numel(), self.base)
+        if self.fused:
+            self.m.slab_finalize_peers(self.y0, self.y1, self.grid_ptrs, recv, recv.numel(),
+                                       self.base)
+        else:
+            self.m.slab_finalize(self.y0, self.y1, miss_slab, recv, recv.numel(), self.base)
         if int(self.m.cfg.buffer_frames) > 1:
             lut, data = self.m.slot_buffers(0)
             bases = [sum(ks[:r]) for r in range(self.P)]

@@ -20,7 +20,7 @@ from tests.gpu_helpers import layers_np
 pytestmark = pytest.mark.gpu
 
 
-def _run(w, P):
+def _run(w, P, peers=False):
     grid = dict(w.grid)
     grid["buffer_frames"] = 1
     f = w.frames[0]
@@ -58,10 +58,14 @@ def _run(w, P):
         states.append((miss_slab, recv))
     assert sum(ks) == ref_data["hits"].shape[0]
     bases = np.concatenate([[0], np.cumsum(ks)])
+    grid_ptrs = [x[1].data_ptr() for x in ranks]  # the ranks' partial miss grids
     for r in range(P):
         m = ranks[r][0]
         miss_slab, recv = states[r]
-        m.slab_finalize(ys[r], ys[r + 1], miss_slab, recv, recv.numel(), int(bases[r]))
+        if peers:  # fused: the finalize sums the P grids itself (no reduce-scatter)
+            m.slab_finalize_peers(ys[r], ys[r + 1], grid_ptrs, recv, recv.numel(), int(bases[r]))
+        else:
+            m.slab_finalize(ys[r], ys[r + 1], miss_slab, recv, recv.numel(), int(bases[r]))
         m.compute_maps_slab(ys[r], ys[r + 1], 0)
     # emulated all-gather of the surface rows
     surf = torch.cat([ranks[r][0].surface()[ys[r]:ys[r + 1]] for r in range(P)])
@@ -92,6 +96,14 @@ def _run(w, P):
 @pytest.mark.parametrize("P", [2, 4])
 def test_slab_partition_c4_matches_single_gpu(P):
     _run(synth.workload(3), P)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_finalize_peers_fused_reduction(P):
+    # NEXT-2 fused collective: gvom_slab_finalize_peers reads the P partial
+    # grids (here P buffers on one GPU standing in for peer memory) and sums
+    # them while encoding the slab -- bit-identical to reduce-scatter + finalize
+    _run(synth.workload(3), P, peers=True)
 
 
 def test_slab_partition_c1_eight_ranks():
