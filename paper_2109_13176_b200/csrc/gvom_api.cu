@@ -573,9 +573,11 @@ static cudaError_t wait_slot_readers(gvom_handle* h, int j) {
 
 // Ray cast a frame: sensors with the same ring count are batched (up to
 // kRayBatch) into one launch with interleaved azimuth tiles.
-static cudaError_t raycast_frame(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
-                                 const std::vector<const float4*>& dptr, const SensorParams* sp,
-                                 uint32_t* miss, uint32_t* bits, const TileCounts& tc) {
+// Sensors with equal ring counts go into one batch (one ray-cast launch and
+// one endpoint launch each, their 32-column tiles interleaved).
+static std::vector<RayBatch> ray_batches(const gvom_scan* scans, int32_t n_scans,
+                                         const std::vector<const float4*>& dptr,
+                                         const SensorParams* sp) {
   std::vector<RayBatch> batches;
   for (int i = 0; i < n_scans; ++i) {
     if (scans[i].n == 0) continue;
@@ -595,6 +597,11 @@ static cudaError_t raycast_frame(gvom_handle* h, const gvom_scan* scans, int32_t
     b->sp[b->S] = sp[i];
     b->S++;
   }
+  return batches;
+}
+
+static cudaError_t raycast_frame(gvom_handle* h, const std::vector<RayBatch>& batches,
+                                 uint32_t* miss, uint32_t* bits, const TileCounts& tc) {
   for (size_t k = 0; k < batches.size(); ++k) {
     const cudaError_t e = stage(h, GVOM_STAGE_RAYCAST, true, [&] {
       return launch_raycast(batches[k], h->d, miss, bits, tc, k + 1 == batches.size(), h->st);
@@ -624,19 +631,16 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     const gvom_status st = stage_points(h, scans, n_scans, dptr);
     if (st != GVOM_OK) return st;
   }
-  GVOM_CU(raycast_frame(h, scans, n_scans, dptr, sp, (uint32_t*)slot.lut, slot.bits, tc));
+  const std::vector<RayBatch> batches = ray_batches(scans, n_scans, dptr, sp);
+  GVOM_CU(raycast_frame(h, batches, (uint32_t*)slot.lut, slot.bits, tc));
   // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
     return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st);
   }));
-  // pass 2b: per-return metrics into the data rows
-  for (int i = 0; i < n_scans; ++i) {
-    const gvom_scan& s = scans[i];
-    if (s.n == 0) continue;
-    GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
-      return launch_endpoint(dptr[i], s.n, s.rings, sp[i], d, slot.lut, slot.data, h->st);
-    }));
-  }
+  // pass 2b: per-return metrics into the data rows, one launch per batch
+  for (const RayBatch& b : batches)
+    GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true,
+                  [&] { return launch_endpoint(b, d, slot.lut, slot.data, h->st); }));
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
   if (h->rolling)  // the frame map joins the window map (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
@@ -1004,7 +1008,7 @@ gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_
   GVOM_CU(cudaMemsetAsync(d_miss, 0, 4 * (size_t)d.V, h->st));
   GVOM_CU(cudaMemsetAsync(cnt, 0, 4 * (size_t)GVOM_MAX_RANKS, h->st));
   TileCounts none{};
-  GVOM_CU(raycast_frame(h, scans, n_scans, dptr, sp, d_miss, nullptr, none));
+  GVOM_CU(raycast_frame(h, ray_batches(scans, n_scans, dptr, sp), d_miss, nullptr, none));
   for (int i = 0; i < n_scans; ++i) {
     const gvom_scan& s = scans[i];
     if (s.n == 0) continue;

@@ -162,8 +162,9 @@ cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, 
 // zeroes a[0:abytes), b[0:bbytes), c[0:cbytes) (multiples of 16, 16-byte aligned)
 cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
                          cudaStream_t st);
-cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                            const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st);
+// per-return hits / min_dz / moments of a sensor batch (same tiling as the ray cast)
+cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lut,
+                            gvom_voxel* data, cudaStream_t st);
 cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                              cudaStream_t st);  // 8-cone variant -> neg directly
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,

@@ -662,12 +662,18 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
 // Returns of azimuth-adjacent lanes often share a voxel (ground near the
 // sensor): runs of equal voxels are reduced with a segmented shuffle
 // reduction and the run head issues the four atomics.
-__global__ void __launch_bounds__(256) k_endpoint(const float4* __restrict__ pts, int64_t n,
-                                                  int32_t rings, const SensorParams sp,
+__global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBatch rb,
                                                   const Dims d, const int32_t* __restrict__ lut,
                                                   gvom_voxel* __restrict__ data) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t p = point_index(tid, rings);
+  // the batch's sensors interleaved by 32-column tile, as in k_raycast
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gt = gtid / rb.tile_threads;
+  const int sidx = (int)(gt % rb.S);
+  const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
+  const int64_t n = rb.n[sidx];
+  const float4* __restrict__ pts = rb.pts[sidx];
+  const SensorParams& sp = rb.sp[sidx];
+  const int64_t p = point_index(tid, rb.rings);
   const int lane = threadIdx.x & 31;
   bool valid = false;
   uint32_t LE = 0xffffffffu, dz = 0u;
@@ -789,12 +795,16 @@ cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, ui
   return cudaGetLastError();
 }
 
-cudaError_t launch_endpoint(const float4* pts, int64_t n, int32_t rings, const SensorParams& sp,
-                            const Dims& d, const int32_t* lut, gvom_voxel* data, cudaStream_t st) {
-  const int64_t threads = point_threads(n, rings);
+cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lut,
+                            gvom_voxel* data, cudaStream_t st) {
+  int64_t tiles = 0;  // per sensor, the batch's maximum
+  for (int s = 0; s < rb.S; ++s) {
+    const int64_t t = (point_threads(rb.n[s], rb.rings) + rb.tile_threads - 1) / rb.tile_threads;
+    tiles = t > tiles ? t : tiles;
+  }
+  const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
-  const int64_t blocks = (threads + 255) / 256;
-  k_endpoint<<<(unsigned)blocks, 256, 0, st>>>(pts, n, rings, sp, d, lut, data);
+  k_endpoint<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(rb, d, lut, data);
   return cudaGetLastError();
 }
 

@@ -58,21 +58,26 @@ def test_step_pageable_host_points_run_eagerly():
 
 
 def test_step_topology_change_reinstantiates():
-    # an empty scan drops its endpoint launch: the graph is re-instantiated and
-    # the results still match the oracle
+    # an empty scan keeps the topology (sensors with equal ring counts share one
+    # ray-cast and one endpoint launch): the cached graph is patched in place.
+    # A scan with another ring count (unordered cloud) adds a batch: the graph
+    # is re-instantiated, and coming back re-instantiates again.  Results match
+    # the oracle throughout.
     w = synth.workload(3)
     f = w.frames[0]
     m = GvomMap(w.grid, max_points_per_frame=f.n_points)
     om = O.OracleMap(w.grid)
     empty = dataclasses.replace(f.scans[1], points=f.scans[1].points[:0])
-    seq = [list(f.scans), [f.scans[0], empty, f.scans[2]], list(f.scans)]
-    for scans in seq:
+    unordered = dataclasses.replace(f.scans[2], rings=0)
+    seq = [(list(f.scans), 1), ([f.scans[0], empty, f.scans[2]], 1),
+           ([f.scans[0], f.scans[1], unordered], 2), (list(f.scans), 3)]
+    for i, (scans, inst) in enumerate(seq):
         om.shift(f.vehicle_xyz)
         om.integrate([(s.points, s.pose) for s in scans])
         m.step(f.vehicle_xyz, [to_dev(s) for s in scans], export=False)
         compare_layers(layers_np(m), om.compute_maps())
-    st = m.graph_stats()
-    assert st["graph_launches"] == 3 and st["instantiations"] == 3, st
+        st = m.graph_stats()
+        assert st["graph_launches"] == i + 1 and st["instantiations"] == inst, (i, st)
 
 
 def test_step_sensor_outside_rejected_before_capture():
