@@ -133,20 +133,23 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
     }
     if (__all_sync(0xffffffffu, zs >= 0 ? z0 >= zc + 32 : !cvalid)) break;
   }
-  // ---- the surface voxel ----
-  const SlotVox v0 = slot_vox(col && zs >= 0, lut, data, cb, zs + dz, d.nz);
-  const uint32_t mn0 = grp_min(v0.mn, lg);
-  // moments of the surface voxel (point spread, NEXT-3)
-  uint64_t sh = 0, s1 = 0, s2 = 0;
+  // ---- the surface voxel: its whole row (counts + moments) in one go ----
+  SlotVox v0{0u, 0u, 0xffffffffu};
+  uint64_t sh = 0, s1 = 0, s2 = 0;  // moments (point spread, NEXT-3)
   if (col && zs >= 0 && (unsigned)(zs + dz) < (unsigned)d.nz) {
     const int32_t r0 = __ldg(lut + cb + zs + dz);
     if (r0 >= 0) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(data + r0));
       const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(data + r0) + 1);
-      sh = v0.h;
+      v0 = SlotVox{a.x, a.y, a.z};
+      sh = a.x;
       s1 = mm.x;
       s2 = mm.y;
+    } else {
+      v0.mi = (uint32_t)(-1 - r0);
     }
   }
+  const uint32_t mn0 = grp_min(v0.mn, lg);
   sh = grp_add64(sh, lg);
   s1 = grp_add64(s1, lg);
   s2 = grp_add64(s2, lg);
@@ -154,36 +157,38 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   const int z_lo = (int)((q_s + lp.T_lo) >> 16);
   const int64_t zh = (q_s + lp.T_hi) >> 16;
   const int z_hi = (int)(zh < (int64_t)d.nz - 1 ? zh : (int64_t)d.nz - 1);
+  // occupied in the merged map (any buffer map): from the 64-z bit window
+  // above z*'s chunk, else (a band wider than the window, not in the shipped
+  // configs) from the maps' LUT cells
+  auto occz = [&](int z) -> bool {
+    const int rel = z - zc;
+    if (rel >= 0 && rel < 64) return (occ >> rel) & 1ull;
+    for (int kk = 0; kk < ss.K; ++kk) {
+      const SlotView& s = ss.s[kk];
+      const int sx = x + s.dx, sy = y + s.dy, uz = z + s.dz;
+      if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny &&
+          (unsigned)uz < (unsigned)d.nz &&
+          __ldg(s.lut + (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy) + uz) >= 0)
+        return true;
+    }
+    return false;
+  };
   uint64_t SH = 0, SW = 0;
   if (zs >= 0) {
     // interior band voxels: certainly in the band when occupied
     for (int z = z_lo + 1; z < z_hi; ++z) {
-      const int rel = z - zc;
-      bool occz;
-      if (rel < 64) {
-        occz = (occ >> rel) & 1ull;
-      } else {  // band wider than the 64-z window (not in the shipped configs)
-        occz = false;
-        for (int kk = 0; kk < ss.K; ++kk) {
-          const SlotView& s = ss.s[kk];
-          const int sx = x + s.dx, sy = y + s.dy, uz = z + s.dz;
-          if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny &&
-              (unsigned)uz < (unsigned)d.nz &&
-              __ldg(s.lut + (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy) + uz) >= 0)
-            occz = true;
-        }
-      }
-      if (!occz) continue;
+      if (!occz(z)) continue;
       const SlotVox v = slot_vox(col, lut, data, cb, z + dz, d.nz);
       SH += v.h;
       SW += (uint64_t)v.h + v.mi;
     }
   }
-  // edge voxels z_lo and z_hi need the merged min_dz (uniform code)
+  // edge voxels z_lo and z_hi need the merged min_dz (uniform code); an edge
+  // voxel that no map occupies contributes nothing and is not loaded
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int z = e == 0 ? z_lo : z_hi;
-    const bool use = zs >= 0 && z <= z_hi && z >= zs && (e == 0 || z_hi != z_lo);
+    const bool use = zs >= 0 && z <= z_hi && z >= zs && (e == 0 || z_hi != z_lo) && occz(z);
     const SlotVox v = use ? slot_vox(col, lut, data, cb, z + dz, d.nz) : SlotVox{0u, 0u, 0xffffffffu};
     const uint32_t mn = grp_min(v.mn, lg);
     if (use && mn != 0xffffffffu) {
