@@ -79,6 +79,26 @@ __device__ __forceinline__ SlotVox slot_vox(bool col, const int32_t* __restrict_
   return r;
 }
 
+// LUT cell of a slot's column at uz; -1 (empty, no misses: contributes
+// nothing) when the column is not in the slot's map or uz is off the grid.
+__device__ __forceinline__ int32_t lut_cell(bool col, const int32_t* __restrict__ lut,
+                                            int64_t cb, int uz, int nz) {
+  return (col && (unsigned)uz < (unsigned)nz) ? __ldg(lut + cb + uz) : -1;
+}
+// The voxel of a LUT cell: data row if occupied, else its miss count.
+__device__ __forceinline__ SlotVox cell_vox(int32_t v, const gvom_voxel* __restrict__ data) {
+  SlotVox r{0u, 0u, 0xffffffffu};
+  if (v >= 0) {
+    const uint4 row = __ldg(reinterpret_cast<const uint4*>(data + v));
+    r.h = row.x;
+    r.mi = row.y;
+    r.mn = row.z;
+  } else {
+    r.mi = (uint32_t)(-1 - v);
+  }
+  return r;
+}
+
 // O7 + O8 fused.  2^lg lanes per output column, lane k <-> buffer map k
 // (32 >> lg columns per warp).  Per column:
 //   z*   : lowest z occupied in any map (OR of the maps' shifted occupancy
@@ -176,11 +196,38 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   uint64_t SH = 0, SW = 0;
   if (zs >= 0) {
     // interior band voxels: certainly in the band when occupied
-    for (int z = z_lo + 1; z < z_hi; ++z) {
-      if (!occz(z)) continue;
-      const SlotVox v = slot_vox(col, lut, data, cb, z + dz, d.nz);
-      SH += v.h;
-      SW += (uint64_t)v.h + v.mi;
+    const int rlo = z_lo + 1 - zc, rhi = z_hi - zc;  // interior rel range [rlo, rhi)
+    if (rlo >= 0 && rhi <= 64) {
+      // occupied interior voxels four at a time: their LUT cells, then their
+      // rows, all in flight together
+      uint64_t mask = rlo < rhi ? occ & ((rhi >= 64 ? ~0ull : (1ull << rhi) - 1ull) &
+                                         ~((1ull << rlo) - 1ull))
+                                : 0ull;
+      while (mask) {
+        int32_t lv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          lv[t] = -1;
+          if (mask) {
+            const int z = zc + __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            lv[t] = lut_cell(col, lut, cb, z + dz, d.nz);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const SlotVox v = cell_vox(lv[t], data);
+          SH += v.h;
+          SW += (uint64_t)v.h + v.mi;
+        }
+      }
+    } else {  // band beyond the 64-z window (not in the shipped configs)
+      for (int z = z_lo + 1; z < z_hi; ++z) {
+        if (!occz(z)) continue;
+        const SlotVox v = slot_vox(col, lut, data, cb, z + dz, d.nz);
+        SH += v.h;
+        SW += (uint64_t)v.h + v.mi;
+      }
     }
   }
   // edge voxels z_lo and z_hi need the merged min_dz (uniform code); an edge

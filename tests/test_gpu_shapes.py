@@ -41,6 +41,8 @@ CASES = [
     (37, 37, 7, 0.5, 1, {"slope_window": 9, "neg_obs_search_cells": 3}),
     (96, 64, 33, 0.2, 2, {"min_obstacle_height": 0.1, "max_obstacle_height": 1.0,
                           "density_threshold": 0.3, "neg_obs_threshold": 0.2}),
+    # obstacle band of 70 voxels: reaches past k_columns' 64-z occupancy window
+    (40, 40, 96, 0.2, 2, {"max_obstacle_height": 14.0}),
 ]
 
 
