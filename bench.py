@@ -98,15 +98,22 @@ def peaks():
 
 
 def measured_traffic(workload: str):
-    """DRAM bytes per k_raycast launch (read + write) for this workload from the
-    committed ncu --set full capture (profiles/raycast_traffic.json), or None."""
+    """DRAM bytes and warp instructions per k_raycast launch for this workload
+    from the committed ncu --set full capture (profiles/raycast_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "raycast_traffic.json")
     try:
         d = json.load(open(p))
         v = d["bytes_per_launch"].get(workload)
-        return (float(v), d["source"][workload]) if v is not None else (None, None)
+        inst = d.get("warp_inst_per_launch", {}).get(workload)
+        return ((float(v) if v is not None else None), d["source"].get(workload),
+                (float(inst) if inst is not None else None))
     except Exception:
-        return None, None
+        return None, None, None
+
+
+# issue peak: 148 SMs x 4 schedulers x one warp instruction per cycle at the
+# measured boost clock (B200_PROFILING.md: 1965 MHz under load)
+ISSUE_PEAK_GINST_S = 148 * 4 * 1.965
 
 
 class ClockSampler:
@@ -467,7 +474,7 @@ def main():
     e2e_value = npts * e2e_steps * world / (e2e_ms / 1e3)
 
     peak, peak_src = peaks()
-    traffic, traffic_src = measured_traffic(w.name)
+    traffic, traffic_src, inst = measured_traffic(w.name)
     ray_ms, ray_n = stage["raycast"]
     ray_launch_ms = ray_ms / max(ray_n, 1)
     scans_per_frame = len(frames[0].scans)
@@ -502,6 +509,14 @@ def main():
                          "traffic_source": traffic_src, "peak_source": peak_src,
                          "launch_ms": ray_launch_ms,
                          "bytes_per_launch": ray_bytes,
+                         "issue": None if inst is None else {
+                             "warp_inst_per_launch": inst,
+                             "achieved_ginst_s": inst / (ray_launch_ms / 1e3) / 1e9,
+                             "peak_ginst_s": ISSUE_PEAK_GINST_S,
+                             "frac": inst / (ray_launch_ms / 1e3) / 1e9 / ISSUE_PEAK_GINST_S,
+                             "note": "the kernel's actual limiter: warp instructions (ncu, "
+                                     "committed capture) / live launch time vs the SM issue "
+                                     "peak; its miss RMWs are L2-resident at this size"},
                          "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)"},
             "integrate": {"ms_per_frame": integ_ms, "points_per_s": npts / (integ_ms / 1e3),
                           "B_int_bytes": B_int, "hbm_frac": B_int / (integ_ms / 1e3) / 1e9 / peak,
