@@ -408,12 +408,15 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
   }
 }
 
-// 64-thread blocks only (launch_raycast): the bound (64, 1) lets ptxas spend 68
-// registers (59 under a 256-thread bound), which measured 8% faster on c5
-// (2.67 vs 2.90 ms) and equal on c2; higher occupancy (40 / 48 warps per SM
-// at 48 / 40 registers) measured slower on every config.
-template <bool kStream>
-__global__ void __launch_bounds__(64, 1) k_raycast(const __grid_constant__ RayBatch rb,
+// Block size: 64 threads (two adjacent rings) when the frame is about one
+// wave of warps -- many small blocks spread long and short rings over the
+// SMs -- and 128 (four adjacent rings) for multi-wave frames, where the
+// locality of adjacent rings wins (c4 / c5: -7% / -4%; c2: +6% with 128).
+// The bound (kBS, 1) lets ptxas spend 68 registers (59 under a 256-thread
+// bound), which measured 8% faster on c5 and equal on c2; higher occupancy
+// (40 / 48 warps per SM at 48 / 40 registers) measured slower on every config.
+template <bool kStream, int kBS>
+__global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayBatch rb,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
@@ -741,18 +744,23 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   }
   const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
-  // small blocks: a frame is about one wave of warps; many small blocks spread
-  // the long (upward / horizontal) and short (ground) rings over the SMs
-  constexpr int bs = 64;
-  const int64_t blocks = (threads + bs - 1) / bs;
+  // block size by frame size (see k_raycast): more than two waves of warps
+  // (148 SMs x 30 resident warps) -> 128 threads, else 64
+  const bool wide = threads / 32 > 2 * 148 * 30;
+  const int bs = wide ? 128 : 64;
+  const unsigned blocks = (unsigned)((threads + bs - 1) / bs);
   // schedule by where the REDs land (see aggregate_red_*): the resident one
   // also needs byte offsets < 2^32
   const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
   const bool stream = !(miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32));
-  if (!stream)
-    k_raycast<false><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+  if (!stream && !wide)
+    k_raycast<false, 64><<<blocks, 64, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+  else if (!stream)
+    k_raycast<false, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+  else if (!wide)
+    k_raycast<true, 64><<<blocks, 64, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   else
-    k_raycast<true><<<(unsigned)blocks, bs, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+    k_raycast<true, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   return cudaGetLastError();
 }
 
