@@ -210,7 +210,7 @@ GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAY
  * as ONE CUDA graph launch: the cached executable graph is patched with the
  * frame's arguments (cudaGraphExecUpdate) or re-instantiated when the launch
  * topology changed.  Falls back to plain stream launches (same kernels) when
- * capture does not apply: pipelined mode, points in pageable
+ * capture does not apply: pipelined mode, points or outputs in pageable
  * host memory, or the stream already under capture by the caller.  The
  * graph and a private capture stream are driver objects held by the handle
  * (released by gvom_destroy); no device memory is allocated.              */

@@ -776,13 +776,17 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
     if (ps != GVOM_OK) return ps;
   }
   // capture needs stream-ordered work only: no cross-call events (pipelined
-  // mode), points on the device or in pinned host memory (stage-timing events
+  // mode), points and outputs on the device or in pinned host memory (stage-timing events
   // become external event-record nodes, see stage()),
   // and a stream that is not already being captured by the caller
   bool graph = !h->pipelined;
   for (int i = 0; graph && i < n_scans; ++i)
     if (scans[i].n > 0 && !is_device_ptr(scans[i].xyzw) && !is_pinned_host_ptr(scans[i].xyzw))
       graph = false;
+  for (int l = 0; graph && dst && l < GVOM_LAYER_COUNT; ++l)  // pageable outputs too
+    if (!is_device_ptr(dst[l]) && !is_pinned_host_ptr(dst[l])) graph = false;
+  if (graph && cost_dst && !is_device_ptr(cost_dst) && !is_pinned_host_ptr(cost_dst))
+    graph = false;
   if (graph) {
     cudaStreamCaptureStatus cs;
     GVOM_CU(cudaStreamIsCapturing(h->st, &cs));

@@ -96,3 +96,27 @@ def test_step_sensor_outside_rejected_before_capture():
     # the handle still works, through the graph
     m.step(f.vehicle_xyz, [to_dev(s) for s in f.scans])
     assert m.graph_stats()["graph_launches"] == 2
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_step_host_outputs(pinned):
+    # host destinations: pinned ones stay in the graph, each layer copied out as
+    # soon as it is final; pageable ones run without a graph; same layers as the
+    # device destinations
+    w = synth.workload(1)
+    f = w.frames[0]
+    scans = [to_dev(s) for s in f.scans]
+    ref = GvomMap(w.grid, max_points_per_frame=f.n_points)
+    _, dev = ref.step(f.vehicle_xyz, scans)
+    ref.synchronize()
+    m = GvomMap(w.grid, max_points_per_frame=f.n_points)
+    host = {k: torch.empty(v.shape, dtype=v.dtype) for k, v in dev.items()}
+    if pinned:
+        host = {k: v.pin_memory() for k, v in host.items()}
+    m.step(f.vehicle_xyz, scans, host)
+    m.synchronize()
+    for k, v in dev.items():
+        assert np.array_equal(np.nan_to_num(host[k].numpy(), nan=-7),
+                              np.nan_to_num(v.cpu().numpy(), nan=-7)), k
+    st = m.graph_stats()
+    assert (st["graph_launches"], st["eager_steps"]) == ((1, 0) if pinned else (0, 1)), st

@@ -6,5 +6,5 @@ for rep in 1 2; do
 for c in $cfgs; do for v in $vars; do
   if [ "$v" = cur ]; then lib=""; else lib=paper_2109_13176_b200/lib/variants/$v.so; fi
   GVOM_LIBRARY=$lib timeout 600 python bench.py --config $c --steps $steps --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | \
-    python -c "import json,sys;d=json.loads(sys.stdin.read());print('AB', '$v', d['config']['workload'][:3], 'step_ms=%.4f'%d['ms_per_step'], 'ray_ms=%.4f'%d['roofline']['launch_ms'], 'frac=%.3f'%d['roofline']['frac'])"
+    python -c "import json,sys;d=json.loads(sys.stdin.read());print('AB', '$v', d['config']['workload'][:3], 'step_ms=%.4f'%d['ms_per_step'], 'ray_ms=%.4f'%d['roofline']['launch_ms'], 'frac=%.3f'%d['roofline']['frac'], 'e2e=%.0f'%(d['e2e']['value']/1e6))"
 done; done; done
