@@ -285,8 +285,10 @@ GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_l
  *     data rows into gvom_slot_buffers(age 0) of every rank, then
  *     gvom_slab_complete(total k): every rank holds the whole frame map;
  *  5. gvom_compute_maps_slab(phase 0): columns of the slab rows; all-gather of
- *     the q_s rows into gvom_surface_buffer(); phase 1: slope, roughness and
- *     negative obstacles for the whole map from the gathered surface.
+ *     the q_s rows into gvom_surface_buffer() (and, with
+ *     GVOM_FLAG_SLOPE_SKIP_OBSTACLES, of the hard / soft rows into
+ *     gvom_obstacle_buffers()); phase 1: slope, roughness and negative
+ *     obstacles for the whole map from the gathered surface.
  * Sums and mins are exact integers, so the result is identical to one GPU.  */
 typedef struct gvom_endpoint {
   uint32_t L;  /* linear voxel index of an in-grid return          */
@@ -329,6 +331,11 @@ GVOM_API gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t 
 GVOM_API gvom_status gvom_map_stream(gvom_handle* h, void** out_stream);
 /* device pointer of the [ny][nx] int32 surface buffer (q_s, INT32_MIN = none) */
 GVOM_API gvom_status gvom_surface_buffer(gvom_handle* h, int32_t** out_d_qs);
+/* device pointers of the [ny][nx] u8 hard / soft layers: with
+ * GVOM_FLAG_SLOPE_SKIP_OBSTACLES the slope windows of phase 1 read them across
+ * slabs, so their rows are all-gathered along with the surface rows        */
+GVOM_API gvom_status gvom_obstacle_buffers(gvom_handle* h, uint8_t** out_d_hard,
+                                           uint8_t** out_d_soft);
 
 /* Instrumentation.  gvom_set_timing(h, mask): every launch of a stage whose
  * bit (1 << GVOM_STAGE_*) is set in mask is bracketed by CUDA events on the

@@ -1185,6 +1185,13 @@ gvom_status gvom_surface_buffer(gvom_handle* h, int32_t** out_d_qs) {
   return GVOM_OK;
 }
 
+gvom_status gvom_obstacle_buffers(gvom_handle* h, uint8_t** out_d_hard, uint8_t** out_d_soft) {
+  if (!h || !out_d_hard || !out_d_soft) return GVOM_E_INVALID;
+  *out_d_hard = h->layers.hard;
+  *out_d_soft = h->layers.soft;
+  return GVOM_OK;
+}
+
 gvom_status gvom_set_timing(gvom_handle* h, int32_t enable) {
   if (!h) return GVOM_E_INVALID;
   h->timing = enable != 0;

@@ -107,6 +107,7 @@ def load_library() -> C.CDLL:
         "gvom_slab_finalize": ([P, I32, I32, P, P, I64, I64], I32),
         "gvom_slot_buffers": ([P, I32, P, P, P], I32),
         "gvom_slab_finalize_peers": ([P, I32, I32, P, I32, P, I64, I64], I32),
+        "gvom_obstacle_buffers": ([P, P, P], I32),
         "gvom_slab_complete": ([P, I64], I32),
         "gvom_compute_maps_slab": ([P, I32, I32, I32], I32),
         "gvom_surface_buffer": ([P, P], I32),
@@ -129,7 +130,8 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_abi_version", "gvom_partial_scan", "gvom_slab_occupancy", "gvom_slab_finalize",
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
-            "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers")
+            "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers",
+            "gvom_obstacle_buffers")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -319,6 +321,18 @@ class GvomMap:
         off = ptr.value - self.workspace.data_ptr()
         n = self.nx * self.ny * 4
         return self.workspace[off:off + n].view(torch.int32).view(self.ny, self.nx)
+
+    def obstacles(self):
+        """(hard, soft): uint8 [ny, nx] views of the library's obstacle layers."""
+        hp, sp_ = C.c_void_p(), C.c_void_p()
+        _check(self.lib.gvom_obstacle_buffers(self.h, C.byref(hp), C.byref(sp_)),
+               "gvom_obstacle_buffers")
+        n = self.nx * self.ny
+        views = []
+        for ptr in (hp, sp_):
+            off = ptr.value - self.workspace.data_ptr()
+            views.append(self.workspace[off:off + n].view(self.ny, self.nx))
+        return tuple(views)
 
     def integrate_scan(self, scans: Iterable[ScanLike]):
         """scans: (points, pose[3,4], rings).  points: float32 [n,4] torch tensor

@@ -156,4 +156,7 @@ class SlabMapper:
     def compute_maps(self):
         self.m.compute_maps_slab(self.y0, self.y1, 0)
         gather_rows(self.m.surface(), self.y0, self.y1, self.group)
+        if int(self.m.cfg.flags) & 2:  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES: windows read them
+            for t in self.m.obstacles():
+                gather_rows(t, self.y0, self.y1, self.group)
         self.m.compute_maps_slab(self.y0, self.y1, 1)

@@ -20,9 +20,10 @@ from tests.gpu_helpers import layers_np
 pytestmark = pytest.mark.gpu
 
 
-def _run(w, P, peers=False):
+def _run(w, P, peers=False, **over):
     grid = dict(w.grid)
     grid["buffer_frames"] = 1
+    grid.update(over)
     f = w.frames[0]
     scans = [(torch.from_numpy(s.points).cuda(), s.pose, s.rings) for s in f.scans]
     # single GPU reference
@@ -67,11 +68,19 @@ def _run(w, P, peers=False):
         else:
             m.slab_finalize(ys[r], ys[r + 1], miss_slab, recv, recv.numel(), int(bases[r]))
         m.compute_maps_slab(ys[r], ys[r + 1], 0)
-    # emulated all-gather of the surface rows
+    # emulated all-gather of the surface rows (+ obstacle rows when slope
+    # windows skip obstacles, as parallel.SlabMapper does)
     surf = torch.cat([ranks[r][0].surface()[ys[r]:ys[r + 1]] for r in range(P)])
+    obst = None
+    if grid.get("slope_skip_obstacles", False):
+        obst = [torch.cat([ranks[r][0].obstacles()[i][ys[r]:ys[r + 1]] for r in range(P)])
+                for i in range(2)]
     for r in range(P):
         m = ranks[r][0]
         m.surface().copy_(surf)
+        if obst is not None:
+            for t, full in zip(m.obstacles(), obst):
+                t.copy_(full)
         m.compute_maps_slab(ys[r], ys[r + 1], 1)
     torch.cuda.synchronize()
     for r in range(P):
@@ -104,6 +113,12 @@ def test_slab_finalize_peers_fused_reduction(P):
     # grids (here P buffers on one GPU standing in for peer memory) and sums
     # them while encoding the slab -- bit-identical to reduce-scatter + finalize
     _run(synth.workload(3), P, peers=True)
+
+
+def test_slab_partition_with_variants():
+    # the slab path with the 8-cone search and obstacle-free slope windows:
+    # phase 1 runs the same surface kernels on the gathered surface
+    _run(synth.workload(3), 2, neg_8cone=True, slope_skip_obstacles=True)
 
 
 def test_slab_partition_c1_eight_ranks():
