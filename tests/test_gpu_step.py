@@ -120,3 +120,15 @@ def test_step_host_outputs(pinned):
                               np.nan_to_num(v.cpu().numpy(), nan=-7)), k
     st = m.graph_stats()
     assert (st["graph_launches"], st["eager_steps"]) == ((1, 0) if pinned else (0, 1)), st
+
+
+def test_step_on_pipelined_handle_with_variants():
+    # GVOM_FLAG_PIPELINE + NEG_8CONE + SLOPE_SKIP_OBSTACLES through gvom_step
+    # (pipelined handles run the step without a graph): frame by frame parity
+    w = synth.config3(speed=4.5, n_frames=5, columns=512)
+    grid = dict(w.grid)
+    grid.update(pipeline=True, neg_8cone=True, slope_skip_obstacles=True)
+    m, _ = run_sequence(synth.Workload(w.name + "_pipe_variants", grid, w.frames, w.world),
+                        use_step=True, check_merged=False)
+    st = m.graph_stats()
+    assert st["eager_steps"] == len(w.frames) and st["graph_launches"] == 0, st
