@@ -1,8 +1,11 @@
 // k_integrate.cu -- pointcloud processing (section III.C) on sm_100a.
 //
-//   raycast  : transform + endpoint occupancy bit + float32 DDA pass-through counts
-//   rank_*   : deterministic rank of occupied voxels in L order (LUT indices)
-//   finalize : in-place LUT encode (rank | -1 - N_m) + data rows
+//   raycast  : transform + endpoint occupancy bit + tile counts + float32 DDA
+//              pass-through counts (the frame's last block scans the tile counts)
+//   finalize : rank of occupied voxels in L order (from the tile offsets) +
+//              in-place LUT encode (rank | -1 - N_m) + data rows; with
+//              peer grids (NEXT-2) it sums the ranks' miss grids as it reads
+//   rank     : single-pass rank over a bitmask (merged-map export path)
 //   endpoint : per-return hits, lowest return, fixed-point moments into data rows
 //
 // Numerics: every float op that decides an integer is written as an explicit
