@@ -253,6 +253,32 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
   k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
 }
 
+// The step loop of a warp: one aggregated red per step, then one DDA step.
+template <bool kStream, class Step>
+__device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uint32_t& L, int left,
+                                          int lane, unsigned after_lanes, Step&& step) {
+  if (kStream) {
+    unsigned act = __ballot_sync(0xffffffffu, left > 0);
+    while (act) {
+      const bool active = left > 0;
+      aggregate_red_stream(miss, L, active, act, after_lanes, lane);
+      step();
+      --left;
+      act = __ballot_sync(0xffffffffu, left > 0);
+    }
+  } else {
+    const bool lane0 = lane == 0;
+    // warp-uniform trip count: lane i is active for its first left_i steps
+    const int Tw = __reduce_max_sync(0xffffffffu, left);
+#pragma unroll 1
+    for (int it = 0; it < Tw; ++it) {
+      const bool active = it < left;
+      aggregate_red_resident(miss, L, active, lane0, after_lanes, lane);
+      step();
+    }
+  }
+}
+
 // The rays of one warp (32 consecutive thread ids gtid of the batch).
 template <bool kStream>
 __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
@@ -389,26 +415,9 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
       atomicAdd(tc.tile + newtile, (uint32_t)__popc(peers));
   }
   const unsigned after_lanes = 0xfffffffeu << lane;  // lanes above this one
-  if (kStream) {
-    unsigned act = __ballot_sync(0xffffffffu, left > 0);
-    while (act) {
-      const bool active = left > 0;
-      aggregate_red_stream(miss, L, active, act, after_lanes, lane);
-      dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
-      --left;
-      act = __ballot_sync(0xffffffffu, left > 0);
-    }
-  } else {
-    const bool lane0 = lane == 0;
-    // warp-uniform trip count: lane i is active for its first left_i steps
-    const int Tw = __reduce_max_sync(0xffffffffu, left);
-#pragma unroll 1
-    for (int it = 0; it < Tw; ++it) {
-      const bool active = it < left;
-      aggregate_red_resident(miss, L, active, lane0, after_lanes, lane);
-      dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
-    }
-  }
+  walk_loop<kStream>(miss, L, left, lane, after_lanes, [&] {
+    dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
+  });
 }
 
 // Block size: 64 threads (two adjacent rings) when the frame is about one
