@@ -317,12 +317,9 @@ def pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier):
     mp_ = GvomMap(gp, max_points_per_frame=npts, device=dev, stream=stream)
     ms_ = mp_.map_stream
 
-    def pstep(i):
+    def pstep(i):  # gvom_step: two graphs per step, fenced by event nodes
         f = frames[i % len(frames)]
-        mp_.shift(f.vehicle_xyz)
-        mp_.integrate_scan(dev_frames[i % len(frames)])
-        mp_.compute_maps()
-        mp_.export_layers(out)
+        mp_.step(f.vehicle_xyz, dev_frames[i % len(frames)], out)
 
     for i in range(args.warmup):
         pstep(i)
@@ -530,8 +527,9 @@ def main():
             "pipelined": None if math.isnan(pipe_ms) else {
                 "value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
                 "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),
-                "note": "GVOM_FLAG_PIPELINE: integrate(t+1) overlaps compute_maps(t); "
-                        "sustained sequence, no L2 flush between steps"},
+                "note": "GVOM_FLAG_PIPELINE through gvom_step (integrate graph on the handle's "
+                        "stream, map graph on the map stream): integrate(t+1) overlaps "
+                        "compute_maps(t); sustained sequence, no L2 flush between steps"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

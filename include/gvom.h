@@ -210,8 +210,11 @@ GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAY
  * as ONE CUDA graph launch: the cached executable graph is patched with the
  * frame's arguments (cudaGraphExecUpdate) or re-instantiated when the launch
  * topology changed.  Falls back to plain stream launches (same kernels) when
- * capture does not apply: pipelined mode, points or outputs in pageable
- * host memory, or the stream already under capture by the caller.  The
+ * capture does not apply: points or outputs in pageable host memory, or the
+ * stream already under capture by the caller.  With GVOM_FLAG_PIPELINE the
+ * step is two graphs -- integrate on the handle's stream, map processing and
+ * export on the map stream -- whose slot fences are external event nodes, so
+ * consecutive steps overlap.  The
  * graph and a private capture stream are driver objects held by the handle
  * (released by gvom_destroy); no device memory is allocated.              */
 GVOM_API gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,

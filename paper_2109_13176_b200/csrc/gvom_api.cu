@@ -187,6 +187,10 @@ struct gvom_handle {
   RollGrid roll{};
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap = nullptr;          // capture stream (the caller's may be legacy)
+  // pipelined handles: the map-processing half of a step is a second graph,
+  // launched on the map stream; cross-step fences are external event nodes
+  cudaGraphExec_t gexec_maps = nullptr;
+  cudaStream_t cap_maps = nullptr;
   bool capturing = false;              // inside gvom_step's capture
   int64_t graph_stats[3] = {0, 0, 0};  // graph launches, instantiations, eager steps
   cudaStream_t ms() const { return pipelined ? mst : st; }
@@ -333,6 +337,46 @@ SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
   return ss;
 }
 
+// Capture body()'s launches with *role (h->st or h->mst) redirected to a
+// private stream (the caller's may be the legacy default stream, which
+// cannot be captured), patch them into *gexec (cudaGraphExecUpdate: same
+// topology, new kernel arguments) or instantiate anew, and launch the graph
+// on the role's real stream.
+template <class F>
+gvom_status capture_launch(gvom_handle* h, cudaStream_t* role, cudaStream_t* cap,
+                                  cudaGraphExec_t* gexec, F&& body) {
+  if (!*cap) GVOM_CU(cudaStreamCreateWithFlags(cap, cudaStreamNonBlocking));
+  cudaStream_t real = *role;
+  GVOM_CU(cudaStreamBeginCapture(*cap, cudaStreamCaptureModeThreadLocal));
+  *role = *cap;
+  h->capturing = true;
+  const gvom_status fs = body();
+  h->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(*cap, &g);
+  *role = real;
+  if (fs != GVOM_OK || ce != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return fs != GVOM_OK ? fs : GVOM_E_CUDA;
+  }
+  if (*gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(*gexec, g, &info) != cudaSuccess) {
+      cudaGetLastError();  // topology changed: instantiate anew
+      cudaGraphExecDestroy(*gexec);
+      *gexec = nullptr;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!*gexec) {
+    e = cudaGraphInstantiate(gexec, g, 0);
+    if (e == cudaSuccess) h->graph_stats[1]++;
+  }
+  cudaGraphDestroy(g);
+  if (e == cudaSuccess) e = cudaGraphLaunch(*gexec, real);
+  return e == cudaSuccess ? GVOM_OK : GVOM_E_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -473,6 +517,8 @@ gvom_status gvom_destroy(gvom_handle* h) {
   if (h->mst) cudaStreamDestroy(h->mst);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->gexec_maps) cudaGraphExecDestroy(h->gexec_maps);
+  if (h->cap_maps) cudaStreamDestroy(h->cap_maps);
   delete h;
   return GVOM_OK;
 }
@@ -568,7 +614,10 @@ static cudaError_t wait_slot_readers(gvom_handle* h, int j) {
   if (!h->pipelined || h->slot_reader[j] < 0) return cudaSuccess;
   int64_t r = h->slot_reader[j];
   if (h->maps_calls - r > gvom_handle::kMapsRing) r = h->maps_calls - gvom_handle::kMapsRing;
-  return cudaStreamWaitEvent(h->st, h->ev_maps[r % gvom_handle::kMapsRing], 0);
+  // under gvom_step's capture: an external wait node (the event is recorded by
+  // an earlier step's map-processing graph)
+  return cudaStreamWaitEvent(h->st, h->ev_maps[r % gvom_handle::kMapsRing],
+                             h->capturing ? cudaEventWaitExternal : 0u);
 }
 
 // Ray cast a frame: sensors with the same ring count are batched (up to
@@ -648,7 +697,9 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     }));
   h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
-  if (h->pipelined) GVOM_CU(cudaEventRecord(h->ev_integrated, h->st));
+  if (h->pipelined)
+    GVOM_CU(cudaEventRecordWithFlags(h->ev_integrated, h->st,
+                                     h->capturing ? cudaEventRecordExternal : 0u));
   return GVOM_OK;
 }
 
@@ -680,7 +731,9 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   const int newest = (h->head - 1 + h->NS) % h->NS;
   int64_t o[3];
   for (int i = 0; i < 3; ++i) o[i] = h->rolling ? h->origin[i] : h->slots[newest].origin[i];
-  if (h->pipelined) GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated, 0));
+  if (h->pipelined)
+    GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated,
+                                h->capturing ? cudaEventWaitExternal : 0u));
   h->lp.o_z = o[2];
   if (h->rolling) {  // the window map at the current origin (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true,
@@ -693,7 +746,8 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   }
   GVOM_CU(surface_layers(h));
   if (h->pipelined)
-    GVOM_CU(cudaEventRecord(h->ev_maps[h->maps_calls % gvom_handle::kMapsRing], h->mst));
+    GVOM_CU(cudaEventRecordWithFlags(h->ev_maps[h->maps_calls % gvom_handle::kMapsRing], h->mst,
+                                     h->capturing ? cudaEventRecordExternal : 0u));
   h->maps_calls++;
   for (int i = 0; i < 3; ++i) h->map_origin[i] = o[i];
   h->maps_valid = true;
@@ -775,11 +829,11 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
     const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
     if (ps != GVOM_OK) return ps;
   }
-  // capture needs stream-ordered work only: no cross-call events (pipelined
-  // mode), points and outputs on the device or in pinned host memory (stage-timing events
-  // become external event-record nodes, see stage()),
-  // and a stream that is not already being captured by the caller
-  bool graph = !h->pipelined;
+  // capture needs stream-ordered work only: points and outputs on the device
+  // or in pinned host memory (stage-timing events and the pipelined fences
+  // become external event nodes), and a stream that is not already being
+  // captured by the caller
+  bool graph = true;
   for (int i = 0; graph && i < n_scans; ++i)
     if (scans[i].n > 0 && !is_device_ptr(scans[i].xyzw) && !is_pinned_host_ptr(scans[i].xyzw))
       graph = false;
@@ -792,9 +846,9 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
     GVOM_CU(cudaStreamIsCapturing(h->st, &cs));
     graph = cs == cudaStreamCaptureStatusNone;
   }
-  auto frame = [&]() -> gvom_status {
-    gvom_status s = gvom_integrate_scan(h, scans, n_scans);
-    if (s == GVOM_OK) s = gvom_compute_maps(h);
+  auto integrate = [&]() -> gvom_status { return gvom_integrate_scan(h, scans, n_scans); };
+  auto maps = [&]() -> gvom_status {
+    gvom_status s = gvom_compute_maps(h);
     if (s == GVOM_OK && dst && cost_weights)
       s = gvom_export_layers_cost(h, dst, dst_bytes, cost_weights, cost_dst, cost_bytes);
     else if (s == GVOM_OK && dst)
@@ -805,43 +859,24 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
   };
   if (!graph) {
     h->graph_stats[2]++;
-    return frame();
+    const gvom_status s = integrate();
+    return s == GVOM_OK ? maps() : s;
   }
-  // capture on the handle's private stream (the caller's stream may be the
-  // legacy default stream, which cannot be captured); the graph is then
-  // launched on the caller's stream
-  if (!h->cap) GVOM_CU(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
-  cudaStream_t user = h->st;
-  GVOM_CU(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-  h->st = h->cap;
-  h->capturing = true;
-  const gvom_status fs = frame();
-  h->capturing = false;
-  cudaGraph_t g = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(h->cap, &g);
-  h->st = user;
-  if (fs != GVOM_OK || ce != cudaSuccess) {
-    if (g) cudaGraphDestroy(g);
-    return fs != GVOM_OK ? fs : GVOM_E_CUDA;
+  if (!h->pipelined) {  // one graph on the handle's stream
+    const gvom_status s = capture_launch(h, &h->st, &h->cap, &h->gexec, [&] {
+      const gvom_status si = integrate();
+      return si == GVOM_OK ? maps() : si;
+    });
+    if (s == GVOM_OK) h->graph_stats[0]++;
+    return s;
   }
-  if (h->gexec) {
-    cudaGraphExecUpdateResultInfo info;
-    if (cudaGraphExecUpdate(h->gexec, g, &info) != cudaSuccess) {
-      cudaGetLastError();  // topology changed (e.g. an empty scan): instantiate anew
-      cudaGraphExecDestroy(h->gexec);
-      h->gexec = nullptr;
-    }
-  }
-  cudaError_t e = cudaSuccess;
-  if (!h->gexec) {
-    e = cudaGraphInstantiate(&h->gexec, g, 0);
-    if (e == cudaSuccess) h->graph_stats[1]++;
-  }
-  cudaGraphDestroy(g);
-  if (e == cudaSuccess) e = cudaGraphLaunch(h->gexec, user);
-  if (e != cudaSuccess) return GVOM_E_CUDA;
-  h->graph_stats[0]++;
-  return GVOM_OK;
+  // pipelined: integrate on the handle's stream, map processing + export on
+  // the map stream, each its own graph (the fences between steps are the
+  // external event nodes recorded / waited inside them)
+  gvom_status s = capture_launch(h, &h->st, &h->cap, &h->gexec, integrate);
+  if (s == GVOM_OK) s = capture_launch(h, &h->mst, &h->cap_maps, &h->gexec_maps, maps);
+  if (s == GVOM_OK) h->graph_stats[0]++;
+  return s;
 }
 
 gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]) {

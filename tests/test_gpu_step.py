@@ -123,12 +123,36 @@ def test_step_host_outputs(pinned):
 
 
 def test_step_on_pipelined_handle_with_variants():
-    # GVOM_FLAG_PIPELINE + NEG_8CONE + SLOPE_SKIP_OBSTACLES through gvom_step
-    # (pipelined handles run the step without a graph): frame by frame parity
-    w = synth.config3(speed=4.5, n_frames=5, columns=512)
+    # GVOM_FLAG_PIPELINE + NEG_8CONE + SLOPE_SKIP_OBSTACLES through gvom_step:
+    # two graphs per step (integrate on the handle's stream, map processing on
+    # the map stream) fenced by external event nodes; frame by frame parity
+    w = synth.config3(speed=4.5, n_frames=10, columns=512)
     grid = dict(w.grid)
     grid.update(pipeline=True, neg_8cone=True, slope_skip_obstacles=True)
     m, _ = run_sequence(synth.Workload(w.name + "_pipe_variants", grid, w.frames, w.world),
                         use_step=True, check_merged=False)
     st = m.graph_stats()
-    assert st["eager_steps"] == len(w.frames) and st["graph_launches"] == 0, st
+    assert st["graph_launches"] == len(w.frames) and st["eager_steps"] == 0, st
+
+
+def test_pipelined_step_graphs_overlap_frames():
+    # back-to-back pipelined steps without synchronisation (the slot fences are
+    # graph event nodes), then every frame's layers checked against the oracle
+    w = synth.config3(speed=12.0, n_frames=12, columns=512)
+    grid = dict(w.grid)
+    grid["pipeline"] = True
+    npts = max(f.n_points for f in w.frames)
+    m = GvomMap(grid, max_points_per_frame=npts)
+    om = O.OracleMap(grid)
+    outs, refs = [], []
+    for f in w.frames:
+        _, lay = m.step(f.vehicle_xyz, [to_dev(s) for s in f.scans])
+        outs.append(lay)
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in f.scans])
+        refs.append(om.compute_maps())
+    m.synchronize()
+    for lay, L in zip(outs, refs):
+        compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
+    st = m.graph_stats()
+    assert st["graph_launches"] == len(w.frames), st
