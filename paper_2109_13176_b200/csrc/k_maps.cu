@@ -683,12 +683,15 @@ __global__ void __launch_bounds__(kTile * kTile) k_negative8(const Dims d, const
 // The same sweep with temporal blocking (TMA lines, 16-byte rows): each
 // consumer warp keeps the keys of kS segments of 32 - 2 kNegH apex positions
 // in registers, plus kNegH halo lanes on each side, and advances them kNegH
-// line steps at a time with shuffles -- no block barrier inside a super-step,
+// line steps at a time with shuffles (kNegH = 4 measured best of 4 / 6 / 8) -- no block barrier inside a super-step,
 // since an error entering at a segment edge moves one lane per line step and
 // never reaches the owned lanes.  Owned keys go through double-buffered shared
 // state once per super-step (one named barrier); a ring slot is released when
 // every consumer warp has arrived on its `empty` barrier.
-constexpr int kNegH = 8;
+#ifndef GVOM_NEG_H
+#define GVOM_NEG_H 4
+#endif
+constexpr int kNegH = GVOM_NEG_H;  // line steps per super-step = halo lanes per side
 constexpr int kNegCore = 32 - 2 * kNegH;
 
 template <int kS>
@@ -1046,8 +1049,8 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   const dim3 grid((unsigned)((A + T - 1) / T), 4);
   // temporally blocked sweep when the rows of both sweep directions are whole
   // 16-byte chunks (TMA) and one segment per warp covers a line (<= 31 warps):
-  // measured faster there (c2 18.4 -> 15.3 us); with 2 / 4 segments per warp
-  // (c4, c5) the per-line-step sweep below measured faster
+  // measured faster there (c2 18.3 -> 15.1 us, c4 29.4 -> 27.0 us); with 2 or
+  // 4 segments per warp (c5) the per-line-step sweep below measured faster
   const int nseg = (int)((NB - 2 + kNegCore - 1) / kNegCore);
   if ((d.nx & 3) == 0 && (d.ny & 3) == 0 && nseg <= 31 && neg_tb_enabled()) {
     const int W = nseg;
