@@ -1048,13 +1048,16 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   }
   const dim3 grid((unsigned)((A + T - 1) / T), 4);
   // temporally blocked sweep when the rows of both sweep directions are whole
-  // 16-byte chunks (TMA) and one segment per warp covers a line (<= 31 warps):
-  // measured faster there (c2 18.3 -> 15.1 us, c4 29.4 -> 27.0 us); with 2 or
-  // 4 segments per warp (c5) the per-line-step sweep below measured faster
+  // 16-byte chunks (TMA) and up to 4 segments per warp (31 warps) cover a
+  // line: c2 18.3 -> 15.1 us, c4 29.4 -> 27.0 us, c5 (2 segments) 110 -> 97 us
   const int nseg = (int)((NB - 2 + kNegCore - 1) / kNegCore);
-  if ((d.nx & 3) == 0 && (d.ny & 3) == 0 && nseg <= 31 && neg_tb_enabled()) {
-    const int W = nseg;
-    auto kern = k_negative_tb<1>;
+#ifndef GVOM_NEG_TB_MAXS
+#define GVOM_NEG_TB_MAXS 4  // segments per warp (A/B knob)
+#endif
+  const int W = nseg < 31 ? nseg : 31;
+  const int S = (nseg + W - 1) / W;
+  if ((d.nx & 3) == 0 && (d.ny & 3) == 0 && S <= GVOM_NEG_TB_MAXS && neg_tb_enabled()) {
+    auto kern = S == 1 ? k_negative_tb<1> : S == 2 ? k_negative_tb<2> : k_negative_tb<4>;
     if (smem > 48 * 1024) {
       const cudaError_t e =
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
