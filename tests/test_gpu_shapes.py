@@ -43,6 +43,9 @@ CASES = [
                           "density_threshold": 0.3, "neg_obs_threshold": 0.2}),
     # obstacle band of 70 voxels: reaches past k_columns' 64-z occupancy window
     (40, 40, 96, 0.2, 2, {"max_obstacle_height": 14.0}),
+    # 1600-wide lines: the cone sweep's temporally blocked kernel with 3-4
+    # segments per warp (k_negative_tb<4>)
+    (1600, 40, 16, 0.25, 1, {}),
 ]
 
 
