@@ -198,6 +198,20 @@ __device__ __forceinline__ void aggregate_red_resident(uint32_t* __restrict__ mi
   const bool brk = prev != key;
   const unsigned heads = __ballot_sync(0xffffffffu, brk);
   const bool head = active && (brk || lane0);
+#ifdef GVOM_RAY_CLZ
+  // run length = clz(brev(heads) & brev(after_lanes)) - lane (clz(0) = 32;
+  // brev(after_lanes) is loop-invariant and hoisted)
+  asm volatile(
+      "{ .reg .pred p; .reg .b32 t;\n\t"
+      "brev.b32 t, %1;\n\t"
+      "and.b32 t, t, %2;\n\t"
+      "clz.b32 t, t;\n\t"
+      "sub.u32 t, t, %3;\n\t"
+      "setp.ne.u32 p, %4, 0;\n\t"
+      "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
+      "r"(heads), "r"(__brev(after_lanes)), "r"(lane), "r"((uint32_t)head));
+  return;
+#endif
   // run length = distance to the next run start above this lane (32 if none):
   // ctz(x) = popc(~x & (x - 1)), which is 32 for x = 0 without a special case
   asm volatile(
@@ -253,6 +267,10 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
   k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
 }
 
+#ifndef GVOM_RAY_UNROLL
+#define GVOM_RAY_UNROLL 1
+#endif
+constexpr int kRayUnroll = GVOM_RAY_UNROLL;
 // The step loop of a warp: one aggregated red per step, then one DDA step.
 template <bool kStream, class Step>
 __device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uint32_t& L, int left,
@@ -270,7 +288,7 @@ __device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uin
     const bool lane0 = lane == 0;
     // warp-uniform trip count: lane i is active for its first left_i steps
     const int Tw = __reduce_max_sync(0xffffffffu, left);
-#pragma unroll 1
+#pragma unroll (kRayUnroll)
     for (int it = 0; it < Tw; ++it) {
       const bool active = it < left;
       aggregate_red_resident(miss, L, active, lane0, after_lanes, lane);
@@ -432,7 +450,21 @@ __global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayB
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
+#ifdef GVOM_RAY_SWZ
+  // block -> work bijection b -> b*P mod G (P coprime to G, near G/phi):
+  // spreads the ring pairs over the SMs of a one-wave frame
+  const uint32_t G = gridDim.x;
+  uint32_t P = (uint32_t)(0.6180339887 * G) | 1u;
+  for (;; P += 2) {
+    uint32_t a = P, b = G;
+    while (b) { const uint32_t t = a % b; a = b; b = t; }
+    if (a == 1 || P >= G) break;
+  }
+  const uint32_t bid = G > 2 ? (uint32_t)(((uint64_t)blockIdx.x * P) % G) : blockIdx.x;
+  ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)bid * blockDim.x + threadIdx.x);
+#else
   ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+#endif
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
 
