@@ -786,6 +786,11 @@ inline int64_t point_threads(int64_t n, int32_t rings) {
 
 }  // namespace
 
+#ifndef GVOM_RAY_NARROW_BS
+#define GVOM_RAY_NARROW_BS 64
+#endif
+constexpr int kRayNarrowBS = GVOM_RAY_NARROW_BS;  // block size of one-wave frames (A/B switch)
+
 cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_grid,
                            uint32_t* bits, const TileCounts& tc, bool last_launch,
                            cudaStream_t st) {
@@ -799,18 +804,20 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   // block size by frame size (see k_raycast): more than two waves of warps
   // (148 SMs x 30 resident warps) -> 128 threads, else 64
   const bool wide = threads / 32 > 2 * 148 * 30;
-  const int bs = wide ? 128 : 64;
+  const int bs = wide ? 128 : kRayNarrowBS;
   const unsigned blocks = (unsigned)((threads + bs - 1) / bs);
   // schedule by where the REDs land (see aggregate_red_*): the resident one
   // also needs byte offsets < 2^32
   const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
   const bool stream = !(miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32));
   if (!stream && !wide)
-    k_raycast<false, 64><<<blocks, 64, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+    k_raycast<false, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss_grid, bits, tc,
+                                                                    last_launch);
   else if (!stream)
     k_raycast<false, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   else if (!wide)
-    k_raycast<true, 64><<<blocks, 64, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+    k_raycast<true, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss_grid, bits, tc,
+                                                                   last_launch);
   else
     k_raycast<true, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
   return cudaGetLastError();
