@@ -15,11 +15,16 @@
  * Each function cites the passage it follows.  The readings of the paper
  * (SURVEY.md 8(c) O0-O11 and the ambiguity ledger A1-A28) are listed in
  * DESIGN.md "Readings".  Pins: tests/test_oracle_*.py.  Parity status:
- *   O0-O8: pinned (closed forms, brute force, invariants, golden G1-G3).
- *   O9   : pinned (closed-form planes, numpy lstsq brute force, G4).
- *   O10  : pinned by special cases / scenario / monotonicity (G5); the cone
- *          geometry itself is "parity unpinned" against the paper (the only
- *          source is the fig:neg_obs_search prose).
+ *   O0-O8: pinned (closed forms, brute force, invariants, golden G1-G3;
+ *          band edges A18 and weighted density A19 by golden G6).
+ *   O9   : pinned (closed-form planes, numpy lstsq brute force, G4; the
+ *          n >= min_plane_points boundary A22 and the 1/n divisor by G6).
+ *   O10  : pinned by special cases / scenario / monotonicity (G5); shared
+ *          ring corners A24 and the strict "larger than" A25 by G6.  The
+ *          cone geometry itself has no paper number (the only source is the
+ *          fig:neg_obs_search prose): it is pinned to reading A24.
+ *   tests/test_oracle_mutants.py checks that each listed misreading fails
+ *   a pin.
  *   Threshold values (T_lo, T_hi, tau, T_neg, N, K_neg): parity unpinned --
  *          the paper gives no values.
  */

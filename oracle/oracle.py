@@ -26,8 +26,10 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "gvom_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# GVOM_ORACLE_SRC: an alternative source file (tests/test_oracle_mutants.py
+# builds deliberately misread copies to check that the pins reject them).
+_SRC = os.environ.get("GVOM_ORACLE_SRC") or os.path.join(_HERE, "gvom_oracle.c")
+_LIB = os.path.join(os.path.dirname(os.path.abspath(_SRC)), "liboracle.so")
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
