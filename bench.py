@@ -170,8 +170,39 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class OneCore:
+    """Pin the calling thread to one host core (the oracle is
+    timed single-threaded, pinned with sched_setaffinity), restored on exit."""
+
+    def __enter__(self):
+        self.prev = None
+        self.core = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = max(self.prev)  # away from core 0 (interrupts, the driver)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            pass
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            try:
+                os.sched_setaffinity(0, self.prev)
+            except OSError:
+                pass
+
+
 def oracle_run(w, budget_s: float, max_frames: int = 1000):
-    """The oracle as it stands on this host (single thread), bounded by budget."""
+    """The oracle as it stands on this host (single thread pinned to one
+    core), bounded by budget."""
+    with OneCore() as oc:
+        r = _oracle_run(w, budget_s, max_frames)
+    r["pinned_core"] = oc.core
+    return r
+
+
+def _oracle_run(w, budget_s: float, max_frames: int = 1000):
     from oracle import oracle as O
     om = O.OracleMap(w.grid)
     t0 = time.perf_counter()
@@ -338,6 +369,33 @@ def pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier):
     return ms
 
 
+def pipelined_e2e_s(w, frames, host_frames, host_outs, npts, dev, stream, steps, args, barrier):
+    """End to end with the pipelined handle: pinned host points in, all layers
+    out to pinned host (two output sets, alternating), steps submitted back to
+    back; wall-clock seconds for `steps` steps up to the final synchronize."""
+    from paper_2109_13176_b200 import GvomMap
+    gp = dict(w.grid)
+    gp["pipeline"] = True
+    mp_ = GvomMap(gp, max_points_per_frame=npts, device=dev, stream=stream)
+
+    def pstep(i):
+        f = frames[i % len(frames)]
+        mp_.step(f.vehicle_xyz, host_frames[i % len(frames)], host_outs[i % 2])
+
+    for i in range(max(3, args.warmup)):
+        pstep(i)
+    mp_.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        pstep(i)
+    mp_.synchronize()
+    dt = time.perf_counter() - t0
+    del mp_
+    barrier()
+    return dt
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -400,7 +458,7 @@ def main():
         # per-stage breakdown comes from a separate instrumented pass below.
         # Timing is on from the warm-up so that the step graph's topology (its
         # event nodes) is instantiated before the timed region.
-        m.set_timing(True, stages=["raycast"])
+        m.set_timing(True, stages=["raycast", "integrate", "maps"])
         for i in range(args.warmup):
             step(i, dev_frames[i % len(frames)], out)
         stream.synchronize()
@@ -446,26 +504,36 @@ def main():
         stream.synchronize()
         barrier()
         e2e_ms = 0.0
+        e2e_wall = 0.0
         for i in range(e2e_steps):
             flush.zero_()
+            stream.synchronize()  # the flush stays outside the wall-clock interval
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
             a.record(stream)
             step(i, host_frames[i % len(frames)], host_out)
             b.record(stream)
             b.synchronize()
+            e2e_wall += time.perf_counter() - t0
             e2e_ms += a.elapsed_time(b)
         barrier()
 
         # ---- pipelined sustained sequence (GVOM_FLAG_PIPELINE) --------
         # (not with the rolling map: GVOM_FLAG_ROLLING excludes pipelining)
-        pipe_ms = float("nan")
+        pipe_ms = pipe_e2e_s = float("nan")
         if not w.grid.get("rolling", False):
             pipe_ms = pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier)
+            host_outs = [host_out, {kk: torch.empty(v.shape, dtype=v.dtype).pin_memory()
+                                    for kk, v in out.items()}]
+            pipe_e2e_s = pipelined_e2e_s(w, frames, host_frames, host_outs, npts, dev, stream,
+                                         e2e_steps, args, barrier)
 
-    t = torch.tensor([total_ms, e2e_ms, pipe_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, e2e_ms, pipe_ms, e2e_wall, pipe_e2e_s], dtype=torch.float64,
+                     device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, e2e_ms, pipe_ms = float(t[0]), float(t[1]), float(t[2])
+    e2e_wall, pipe_e2e_s = float(t[3]), float(t[4])
     pts_total = npts * args.steps * world
     value = pts_total / (total_ms / 1e3)
     e2e_value = npts * e2e_steps * world / (e2e_ms / 1e3)
@@ -479,11 +547,12 @@ def main():
     ray_bytes = (16 * npts + 8 * Mi + 8 * H) / launches_per_frame  # per launch
     ray_gbs = ray_bytes / (ray_launch_ms / 1e3) / 1e9
     V = m.nx * m.ny * m.nz
-    integ_keys = ("memset", "raycast", "rank_count", "rank_scan", "finalize", "endpoint")
-    integ_ms = sum(stage_all[s][0] for s in integ_keys) / n_inst
+    # integrate / compute_maps: one event pair around each whole call inside
+    # the timed, graphed steps (GVOM_STAGE_INTEGRATE / _MAPS)
+    integ_ms = stage["integrate"][0] / max(stage["integrate"][1], 1)
     B_int = 16 * npts + 48 * H + 8 * Mi + 4 * V
     K = int(w.grid["buffer_frames"])
-    maps_ms = sum(stage_all[s][0] for s in ("columns", "slope", "negative")) / n_inst
+    maps_ms = stage["maps"][0] / max(stage["maps"][1], 1)
 
     if rank == 0:
         cpu = None
@@ -517,13 +586,28 @@ def main():
                          "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)"},
             "integrate": {"ms_per_frame": integ_ms, "points_per_s": npts / (integ_ms / 1e3),
                           "B_int_bytes": B_int, "hbm_frac": B_int / (integ_ms / 1e3) / 1e9 / peak,
-                          "H": H, "M": Mi, "k": k},
+                          "H": H, "M": Mi, "k": k,
+                          "timing": "events around gvom_integrate_scan inside the timed graphed "
+                                    "steps (GVOM_STAGE_INTEGRATE)"},
             "compute_maps_ms": maps_ms,
+            "compute_maps_timing": "events around gvom_compute_maps inside the timed graphed "
+                                   "steps (GVOM_STAGE_MAPS)",
             "stages_ms_per_step": {s: v[0] / n_inst for s, v in stage_all.items() if v[1]},
             "stages_note": "separate instrumented pass (events around every launch, "
                            "separate calls without a graph)",
             "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * npts,
-                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 5 + 3), "steps": e2e_steps},
+                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 5 + 3), "steps": e2e_steps,
+                    "timing": "CUDA events around each gvom_step (pinned host points in, 8 "
+                              "layers out to pinned host), synchronised every step",
+                    "wall_value": npts * e2e_steps * world / e2e_wall,
+                    "wall_timing": "perf_counter around the host call + synchronize (host "
+                                   "submit and ctypes marshalling included; L2 flush outside)",
+                    "pipelined_value": (None if math.isnan(pipe_e2e_s)
+                                        else npts * e2e_steps * world / pipe_e2e_s),
+                    "pipelined_timing": "GVOM_FLAG_PIPELINE handle, same host buffers in and "
+                                        "out (outputs double-buffered), steps submitted back "
+                                        "to back, wall clock over the sequence to the final "
+                                        "synchronize"},
             "pipelined": None if math.isnan(pipe_ms) else {
                 "value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
                 "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),

@@ -227,6 +227,15 @@ GVOM_API gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], cons
  * out[2] steps run without a graph.                                        */
 GVOM_API gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]);
 
+/* Test hook (fault injection).  GVOM_FAULT_CAPTURE: the next gvom_step
+ * capture fails as if cudaStreamEndCapture had failed; the step returns
+ * GVOM_E_CUDA and the map state (buffer ring, slot origins, map-processing
+ * bookkeeping) is rolled back to before the step's integrate, so the next
+ * step continues as if the failed one had never been called (its shift
+ * stands).  0 clears a pending fault.                                      */
+#define GVOM_FAULT_CAPTURE 1
+GVOM_API gvom_status gvom_debug_inject_fault(gvom_handle* h, int32_t what);
+
 /* Costmap ("each of the output maps get some weight assigned to them
  * and the resulting per pixel sum is the cost in that pixel"; SURVEY 8(f)
  * NEXT-4).  cost = w0*hard + w1*soft + w2*density + w3*negative + w4*slope
@@ -346,10 +355,14 @@ GVOM_API gvom_status gvom_obstacle_buffers(gvom_handle* h, uint8_t** out_d_hard,
  * returns, per stage, [total ms, launches] pairs (2*GVOM_STAGE_COUNT
  * doubles), then clears the record.  gvom_launch_count returns the number of
  * kernels this handle has launched so far.                                  */
+/* GVOM_STAGE_INTEGRATE / GVOM_STAGE_MAPS bracket a whole gvom_integrate_scan /
+ * gvom_compute_maps call (one event pair around all its launches, recorded
+ * inside gvom_step's graph too) instead of every launch.                   */
 enum {
   GVOM_STAGE_RAYCAST = 0, GVOM_STAGE_RANK_COUNT, GVOM_STAGE_RANK_SCAN, GVOM_STAGE_FINALIZE,
   GVOM_STAGE_ENDPOINT, GVOM_STAGE_COLUMNS, GVOM_STAGE_SLOPE, GVOM_STAGE_NEGATIVE,
-  GVOM_STAGE_MEMSET, GVOM_STAGE_H2D, GVOM_STAGE_EXPORT, GVOM_STAGE_MERGE, GVOM_STAGE_COUNT
+  GVOM_STAGE_MEMSET, GVOM_STAGE_H2D, GVOM_STAGE_EXPORT, GVOM_STAGE_MERGE,
+  GVOM_STAGE_INTEGRATE, GVOM_STAGE_MAPS, GVOM_STAGE_COUNT
 };
 GVOM_API gvom_status gvom_set_timing(gvom_handle* h, int32_t enable);
 GVOM_API gvom_status gvom_stage_times(gvom_handle* h, double* out, int32_t n_doubles);

@@ -19,7 +19,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libgvom.so")
 SOURCES = ["k_integrate.cu", "k_maps.cu", "k_slab.cu", "k_roll.cu", "gvom_api.cu"]
-HEADERS = ["gvom_internal.cuh"]
+HEADERS = ["gvom_internal.cuh", "gvom_device.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -10,9 +10,20 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gvom_internal.cuh"
 
 using namespace gvom;
+
+namespace {
+// NVTX range over a host call (SURVEY 5 tracing): names the stage in nsys /
+// ncu timelines; a no-op unless a tool is attached (header-only NVTX v3).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -80,6 +91,8 @@ Dims make_dims(const gvom_config* c) {
   d.nz = c->nz;
   d.V = (int64_t)c->nx * c->ny * c->nz;
   d.W = (d.V + 31) / 32;
+  d.sms = 148;
+  d.l2_bytes = 126500000;
   return d;
 }
 
@@ -193,6 +206,7 @@ struct gvom_handle {
   cudaStream_t cap_maps = nullptr;
   bool capturing = false;              // inside gvom_step's capture
   int64_t graph_stats[3] = {0, 0, 0};  // graph launches, instantiations, eager steps
+  int32_t fault = 0;                   // gvom_debug_inject_fault (tests)
   cudaStream_t ms() const { return pipelined ? mst : st; }
 };
 
@@ -229,6 +243,36 @@ cudaError_t stage(gvom_handle* h, int id, bool is_kernel, F&& f, cudaStream_t on
   if (is_kernel && e == cudaSuccess) h->launches++;
   return e;
 }
+
+// Event bracket around a whole call (GVOM_STAGE_INTEGRATE / _MAPS): times the
+// call's launches as they run back to back (inside a step graph too), without
+// the per-launch events of the kernel stages.
+struct Bracket {
+  gvom_handle* h;
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  Bracket(gvom_handle* h_, int id_, cudaStream_t s_) : h(h_), id(id_), s(s_) {
+    if (h->timing && ((h->timing_mask >> id) & 1u)) {
+      a = take_event(h);
+      if (a) cudaEventRecordWithFlags(a, s, h->capturing ? cudaEventRecordExternal : 0u);
+    }
+  }
+  void end() {
+    if (!a) return;
+    cudaEvent_t b = take_event(h);
+    if (b) {
+      cudaEventRecordWithFlags(b, s, h->capturing ? cudaEventRecordExternal : 0u);
+      h->recs.push_back({id, a, b});
+    } else {
+      h->pool.push_back(a);
+    }
+    a = nullptr;
+  }
+  ~Bracket() {
+    if (a) h->pool.push_back(a);  // the call failed: no record
+  }
+};
 
 void snap(const gvom_config& c, const double p[3], int64_t o[3]) {
   // reading A3: o = floor(p/res + 0.5) - (nx/2, ny/2, floor(nz * frac))
@@ -337,6 +381,49 @@ SlotSet buffer_slots(gvom_handle* h, const int64_t o_out[3]) {
   return ss;
 }
 
+// Host-side state a step advances while its launches are captured (the ring
+// head and count, slot origins, the map-processing bookkeeping).  Restored
+// when the capture, instantiation or graph launch fails: none of the captured
+// work ran, so the ring must not name a slot whose frame was never written.
+struct HostState {
+  int head = 0, count = 0;
+  std::vector<int64_t> slot_origin;
+  std::vector<int64_t> slot_reader;
+  int64_t maps_calls = 0, map_origin[3] = {0, 0, 0}, o_z = 0;
+  bool maps_valid = false;
+  SlotSet map_slots{};
+  uint64_t rank_calls = 0;
+};
+
+HostState save_state(const gvom_handle* h) {
+  HostState s;
+  s.head = h->head;
+  s.count = h->count;
+  for (const Slot& sl : h->slots) s.slot_origin.insert(s.slot_origin.end(), sl.origin, sl.origin + 3);
+  s.slot_reader = h->slot_reader;
+  s.maps_calls = h->maps_calls;
+  for (int i = 0; i < 3; ++i) s.map_origin[i] = h->map_origin[i];
+  s.o_z = h->lp.o_z;
+  s.maps_valid = h->maps_valid;
+  s.map_slots = h->map_slots;
+  s.rank_calls = h->rank_calls;
+  return s;
+}
+
+void restore_state(gvom_handle* h, const HostState& s) {
+  h->head = s.head;
+  h->count = s.count;
+  for (size_t k = 0; k < h->slots.size(); ++k)
+    for (int i = 0; i < 3; ++i) h->slots[k].origin[i] = s.slot_origin[3 * k + i];
+  h->slot_reader = s.slot_reader;
+  h->maps_calls = s.maps_calls;
+  for (int i = 0; i < 3; ++i) h->map_origin[i] = s.map_origin[i];
+  h->lp.o_z = s.o_z;
+  h->maps_valid = s.maps_valid;
+  h->map_slots = s.map_slots;
+  h->rank_calls = s.rank_calls;
+}
+
 // Capture body()'s launches with *role (h->st or h->mst) redirected to a
 // private stream (the caller's may be the legacy default stream, which
 // cannot be captured), patch them into *gexec (cudaGraphExecUpdate: same
@@ -347,16 +434,22 @@ gvom_status capture_launch(gvom_handle* h, cudaStream_t* role, cudaStream_t* cap
                                   cudaGraphExec_t* gexec, F&& body) {
   if (!*cap) GVOM_CU(cudaStreamCreateWithFlags(cap, cudaStreamNonBlocking));
   cudaStream_t real = *role;
+  const HostState saved = save_state(h);
   GVOM_CU(cudaStreamBeginCapture(*cap, cudaStreamCaptureModeThreadLocal));
   *role = *cap;
   h->capturing = true;
   const gvom_status fs = body();
   h->capturing = false;
   cudaGraph_t g = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(*cap, &g);
+  cudaError_t ce = cudaStreamEndCapture(*cap, &g);
   *role = real;
+  if (h->fault == GVOM_FAULT_CAPTURE) {  // test hook: as if EndCapture had failed
+    h->fault = 0;
+    ce = cudaErrorStreamCaptureInvalidated;
+  }
   if (fs != GVOM_OK || ce != cudaSuccess) {
     if (g) cudaGraphDestroy(g);
+    restore_state(h, saved);
     return fs != GVOM_OK ? fs : GVOM_E_CUDA;
   }
   if (*gexec) {
@@ -374,7 +467,12 @@ gvom_status capture_launch(gvom_handle* h, cudaStream_t* role, cudaStream_t* cap
   }
   cudaGraphDestroy(g);
   if (e == cudaSuccess) e = cudaGraphLaunch(*gexec, real);
-  return e == cudaSuccess ? GVOM_OK : GVOM_E_CUDA;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    restore_state(h, saved);
+    return GVOM_E_CUDA;
+  }
+  return GVOM_OK;
 }
 
 }  // namespace
@@ -413,6 +511,16 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   if (!h) return GVOM_E_NOMEM;
   h->cfg = *cfg;
   h->d = make_dims(cfg);
+  {  // the current device's SM count and L2 size (launch heuristics)
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+        h->d.sms = v;
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess && v > 0)
+        h->d.l2_bytes = v;
+    }
+    cudaGetLastError();
+  }
   h->lay = lay;
   h->st = (cudaStream_t)cuda_stream;
   h->ws = (char*)d_workspace;
@@ -537,6 +645,7 @@ gvom_status gvom_synchronize(gvom_handle* h) {
 }
 
 gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int64_t out_delta[3]) {
+  NvtxRange nvtx_("gvom_shift");
   if (!h || !vehicle_xyz) return GVOM_E_INVALID;
   for (int i = 0; i < 3; ++i)
     if (!isfinite(vehicle_xyz[i])) return GVOM_E_INVALID;
@@ -661,16 +770,18 @@ static cudaError_t raycast_frame(gvom_handle* h, const std::vector<RayBatch>& ba
 }
 
 gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
+  NvtxRange nvtx_("gvom_integrate_scan");
   SensorParams sp[GVOM_MAX_SENSORS];
   const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
   if (ps != GVOM_OK) return ps;
   Slot& slot = h->slots[h->head];
   const Dims& d = h->d;
   GVOM_CU(wait_slot_readers(h, h->head));
+  Bracket br(h, GVOM_STAGE_INTEGRATE, h->st);
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
     return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
                         (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
-                        h->lay.tilecnt_bytes, h->st);
+                        h->lay.tilecnt_bytes, h->d, h->st);
   }));
   // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
   TileCounts tc = h->tc;
@@ -695,6 +806,7 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
       return launch_roll_accumulate(h->roll, d, slot.lut, slot.data, h->st);
     }));
+  br.end();
   h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
   if (h->pipelined)
@@ -726,6 +838,7 @@ static cudaError_t surface_layers(gvom_handle* h) {
 }
 
 gvom_status gvom_compute_maps(gvom_handle* h) {
+  NvtxRange nvtx_("gvom_compute_maps");
   if (!h) return GVOM_E_INVALID;
   if (h->count == 0) return GVOM_E_EMPTY;
   const int newest = (h->head - 1 + h->NS) % h->NS;
@@ -735,6 +848,7 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
     GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated,
                                 h->capturing ? cudaEventWaitExternal : 0u));
   h->lp.o_z = o[2];
+  Bracket br(h, GVOM_STAGE_MAPS, h->ms());
   if (h->rolling) {  // the window map at the current origin (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true,
                   [&] { return launch_columns_roll(h->roll, h->d, h->lp, h->layers, h->st); }));
@@ -745,6 +859,7 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
         [&] { return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->ms()); }, h->ms()));
   }
   GVOM_CU(surface_layers(h));
+  br.end();
   if (h->pipelined)
     GVOM_CU(cudaEventRecordWithFlags(h->ev_maps[h->maps_calls % gvom_handle::kMapsRing], h->mst,
                                      h->capturing ? cudaEventRecordExternal : 0u));
@@ -771,6 +886,7 @@ static const void* layer_src(gvom_handle* h, int layer, size_t* elem) {
 
 gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
                                const size_t dst_bytes[GVOM_LAYER_COUNT]) {
+  NvtxRange nvtx_("gvom_export_layers");
   if (!h || !dst || !dst_bytes) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
   CopyJob job;
@@ -807,6 +923,7 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
                       int32_t n_scans, void* const dst[GVOM_LAYER_COUNT],
                       const size_t dst_bytes[GVOM_LAYER_COUNT], const float cost_weights[7],
                       void* cost_dst, size_t cost_bytes, int64_t out_delta[3]) {
+  NvtxRange nvtx_("gvom_step");
   if (!h || !vehicle_xyz) return GVOM_E_INVALID;
   if (dst && !dst_bytes) return GVOM_E_INVALID;
   if ((cost_weights == nullptr) != (cost_dst == nullptr)) return GVOM_E_INVALID;
@@ -879,6 +996,12 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
   return s;
 }
 
+gvom_status gvom_debug_inject_fault(gvom_handle* h, int32_t what) {
+  if (!h || (what != 0 && what != GVOM_FAULT_CAPTURE)) return GVOM_E_INVALID;
+  h->fault = what;
+  return GVOM_OK;
+}
+
 gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]) {
   if (!h || !out) return GVOM_E_INVALID;
   for (int i = 0; i < 3; ++i) out[i] = h->graph_stats[i];
@@ -886,6 +1009,7 @@ gvom_status gvom_graph_stats(gvom_handle* h, int64_t out[3]) {
 }
 
 gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t dst_bytes) {
+  NvtxRange nvtx_("gvom_export_2d");
   if (!h || !dst) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
   size_t elem;
@@ -900,6 +1024,7 @@ gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t d
 }
 
 gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst, size_t dst_bytes) {
+  NvtxRange nvtx_("gvom_costmap");
   if (!h || !weights || !dst) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
   const size_t bytes = 4 * (size_t)h->lay.cells;
@@ -922,6 +1047,7 @@ gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst, size
 gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT],
                                    const size_t dst_bytes[GVOM_LAYER_COUNT],
                                    const float weights[7], void* cost_dst, size_t cost_bytes) {
+  NvtxRange nvtx_("gvom_export_layers_cost");
   if (!h || !dst || !dst_bytes || !weights || !cost_dst) return GVOM_E_INVALID;
   if (!h->maps_valid) return GVOM_E_EMPTY;
   CostWeights cw;
@@ -971,6 +1097,7 @@ gvom_status gvom_map_origin(gvom_handle* h, int64_t out_origin[3]) {
 
 gvom_status gvom_export_voxels(gvom_handle* h, int32_t* d_lut, gvom_voxel* d_data, int64_t cap,
                                int64_t* out_k) {
+  NvtxRange nvtx_("gvom_export_voxels");
   if (!h || !d_lut || !out_k || cap < 0 || (cap > 0 && !d_data)) return GVOM_E_INVALID;
   if (h->rolling) return GVOM_E_INVALID;  // see gvom_export_window
   if (!h->maps_valid) return GVOM_E_EMPTY;
@@ -1024,6 +1151,7 @@ static bool slab_ok(const gvom_handle* h, int32_t y0, int32_t y1) {
 gvom_status gvom_partial_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
                               uint32_t* d_miss, gvom_endpoint* d_ep, int64_t ep_cap,
                               const int32_t* slab_y, int32_t n_ranks, int64_t* out_counts) {
+  NvtxRange nvtx_("gvom_partial_scan");
   if (!h || !d_miss || !slab_y || !out_counts || n_ranks < 1 || n_ranks > GVOM_MAX_RANKS ||
       ep_cap < 0 || (ep_cap > 0 && !d_ep) || h->rolling)
     return GVOM_E_INVALID;
@@ -1085,12 +1213,13 @@ static void slab_tiles(const gvom_handle* h, int32_t y0, int32_t y1, int64_t* t0
 
 gvom_status gvom_slab_occupancy(gvom_handle* h, int32_t y0, int32_t y1, const gvom_endpoint* d_ep,
                                 int64_t n_ep, int64_t* out_k) {
+  NvtxRange nvtx_("gvom_slab_occupancy");
   if (!slab_ok(h, y0, y1) || !out_k || n_ep < 0 || (n_ep > 0 && !d_ep)) return GVOM_E_INVALID;
   Slot& slot = h->slots[h->head];
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
     return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
                         (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
-                        h->lay.tilecnt_bytes, h->st);
+                        h->lay.tilecnt_bytes, h->d, h->st);
   }));
   GVOM_CU(stage(h, GVOM_STAGE_RANK_COUNT, true, [&] {
     return launch_slab_bits((const EpRecord*)d_ep, n_ep, slot.bits, h->tc.tile, h->st);
@@ -1147,6 +1276,7 @@ static gvom_status slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
 
 gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uint32_t* d_miss_slab,
                                const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  NvtxRange nvtx_("gvom_slab_finalize");
   if (!d_miss_slab) return GVOM_E_INVALID;
   return slab_finalize(h, y0, y1, d_miss_slab, nullptr, d_ep, n_ep, base);
 }
@@ -1154,6 +1284,7 @@ gvom_status gvom_slab_finalize(gvom_handle* h, int32_t y0, int32_t y1, const uin
 gvom_status gvom_slab_finalize_peers(gvom_handle* h, int32_t y0, int32_t y1,
                                      const uint32_t* const* d_miss_grids, int32_t n_grids,
                                      const gvom_endpoint* d_ep, int64_t n_ep, int64_t base) {
+  NvtxRange nvtx_("gvom_slab_finalize_peers");
   if (!d_miss_grids || n_grids < 1 || n_grids > GVOM_MAX_RANKS) return GVOM_E_INVALID;
   PeerGrids pg{};
   pg.P = n_grids;
@@ -1175,6 +1306,7 @@ gvom_status gvom_slot_buffers(gvom_handle* h, int32_t age, int32_t** out_d_lut,
 }
 
 gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total) {
+  NvtxRange nvtx_("gvom_slab_complete");
   if (!h || h->pipelined || h->rolling || h->count == 0 || k_total < 0 || k_total > h->lay.cap)
     return GVOM_E_INVALID;
   Slot& slot = h->slots[(h->head - 1 + h->NS) % h->NS];
@@ -1186,6 +1318,7 @@ gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total) {
 }
 
 gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32_t phase) {
+  NvtxRange nvtx_("gvom_compute_maps_slab");
   if (!slab_ok(h, y0, y1) || (phase != 0 && phase != 1)) return GVOM_E_INVALID;
   if (h->count == 0) return GVOM_E_EMPTY;
   if (phase == 0) {

@@ -27,6 +27,10 @@ struct Dims {
   int32_t nx, ny, nz;
   int64_t V;  // nx*ny*nz
   int64_t W;  // bitmask words = ceil(V/32)
+  // the device the handle runs on (queried in gvom_create; the B200 values
+  // until then): launch heuristics derive their thresholds from these
+  int32_t sms;       // multiprocessors (B200: 148)
+  int64_t l2_bytes;  // L2 cache size (B200: 126.5 MB)
 };
 
 // One buffer map ("lookup array, data array, map origin").
@@ -161,7 +165,7 @@ cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, 
                         uint32_t* total, cudaStream_t st);
 // zeroes a[0:abytes), b[0:bbytes), c[0:cbytes) (multiples of 16, 16-byte aligned)
 cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
-                         cudaStream_t st);
+                         const Dims& d, cudaStream_t st);
 // per-return hits / min_dz / moments of a sensor batch (same tiling as the ray cast)
 cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lut,
                             gvom_voxel* data, cudaStream_t st);

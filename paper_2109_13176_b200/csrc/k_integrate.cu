@@ -16,13 +16,11 @@
 #include <cuda/atomic>
 #include <stdlib.h>
 
-#include "gvom_internal.cuh"
+#include "gvom_device.cuh"
 
 namespace gvom {
 
 namespace {
-
-constexpr float kGLim = 4194304.0f;  // |g_i| < 2^22 voxels (reading A5)
 
 __device__ __forceinline__ int64_t point_index(int64_t tid, int32_t rings) {
   // Sensor-order scans (column-major, beam-fastest): lane l of a warp takes
@@ -37,25 +35,6 @@ __device__ __forceinline__ int64_t point_index(int64_t tid, int32_t rings) {
   const int32_t r = w >> 5;
   const int32_t l = w & 31;
   return (tile * 32 + l) * rings + r;
-}
-
-// O3: g_i = ((A_i0 x + A_i1 y) + A_i2 z) + b_i, f32 RN each, no contraction.
-__device__ __forceinline__ bool transform_point(const SensorParams& sp, const float4 p,
-                                                float& g0, float& g1, float& g2) {
-  if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) return false;
-  if (p.x == 0.0f && p.y == 0.0f && p.z == 0.0f) return false;
-  float g[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const float t0 = __fmul_rn(sp.A[3 * i + 0], p.x);
-    const float t1 = __fmul_rn(sp.A[3 * i + 1], p.y);
-    const float t2 = __fmul_rn(sp.A[3 * i + 2], p.z);
-    g[i] = __fadd_rn(__fadd_rn(__fadd_rn(t0, t1), t2), sp.b[i]);
-  }
-  g0 = g[0];
-  g1 = g[1];
-  g2 = g[2];
-  return fabsf(g0) < kGLim && fabsf(g1) < kGLim && fabsf(g2) < kGLim;
 }
 
 // Exact O5 walk of one ray, oracle control flow verbatim (slow path for the
@@ -126,7 +105,6 @@ __device__ __forceinline__ bool after(float k, int a, float K, int A) {
 // walk's end; then it runs T ungated argmin steps.  Rays failing the check or
 // with a non-finite 1/d take the exact slow path.  The rule is restated and
 // checked against the oracle in tests/test_dda_fastpath_rule.py.
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane);
 
 // The frame's last finishing ray-cast block (of the last sensor's launch)
 // turns the tile counts into exclusive offsets: each thread sums a
@@ -240,10 +218,11 @@ __device__ __forceinline__ void aggregate_red_stream(uint32_t* __restrict__ miss
 }
 
 #ifndef GVOM_RAY_STREAM_BYTES
-#define GVOM_RAY_STREAM_BYTES (int64_t(64) << 20)
+#define GVOM_RAY_STREAM_BYTES 0
 #endif
-// miss grids above this size take the streaming schedule (B200 L2: 126 MB,
-// split over two dies; tuned on c4 / c5)
+// miss grids above half the L2 (B200: 126 MB split over two dies, so 64 MB;
+// tuned on c4 / c5) take the streaming schedule; a nonzero
+// GVOM_RAY_STREAM_BYTES overrides the threshold (A/B builds)
 constexpr int64_t kRayStreamBytes = GVOM_RAY_STREAM_BYTES;
 
 // One DDA step (O5): argmin of the three keys, strict <, ties to the lowest
@@ -466,15 +445,6 @@ __global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayB
   ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
 #endif
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
 }
 
 // Single-pass rank of the occupied voxels (decoupled look-back scan over the
@@ -802,14 +772,15 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
   // block size by frame size (see k_raycast): more than two waves of warps
-  // (148 SMs x 30 resident warps) -> 128 threads, else 64
-  const bool wide = threads / 32 > 2 * 148 * 30;
+  // (SMs x 30 resident warps) -> 128 threads, else 64
+  const bool wide = threads / 32 > 2 * (int64_t)d.sms * 30;
   const int bs = wide ? 128 : kRayNarrowBS;
   const unsigned blocks = (unsigned)((threads + bs - 1) / bs);
   // schedule by where the REDs land (see aggregate_red_*): the resident one
   // also needs byte offsets < 2^32
   const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
-  const bool stream = !(miss_bytes <= kRayStreamBytes && miss_bytes < (int64_t(1) << 32));
+  const int64_t resident_max = kRayStreamBytes > 0 ? kRayStreamBytes : d.l2_bytes / 2;
+  const bool stream = !(miss_bytes <= resident_max && miss_bytes < (int64_t(1) << 32));
   if (!stream && !wide)
     k_raycast<false, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss_grid, bits, tc,
                                                                     last_launch);
@@ -832,16 +803,14 @@ cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, 
   return cudaGetLastError();
 }
 
-// miss grids zeroed write-back: (32 MiB, 96 MiB] (B200 L2: 126 MB)
-constexpr size_t kZeroKeepMinBytes = size_t(32) << 20, kZeroKeepMaxBytes = size_t(96) << 20;
-
+// miss grids zeroed write-back: (L2/4, 3 L2/4] (B200, 126 MB: ~32-95 MB)
 cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c, size_t cbytes,
-                         cudaStream_t st) {
+                         const Dims& d, cudaStream_t st) {
   const int64_t n = (int64_t)(abytes / 16 + bbytes / 16 + cbytes / 16);
   int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > (int64_t)d.sms * 8) blocks = (int64_t)d.sms * 8;
   if (blocks < 1) blocks = 1;
-  const bool keep_a = abytes > kZeroKeepMinBytes && abytes <= kZeroKeepMaxBytes;
+  const bool keep_a = (int64_t)abytes > d.l2_bytes / 4 && (int64_t)abytes <= 3 * d.l2_bytes / 4;
   k_zero3<<<(unsigned)blocks, 256, 0, st>>>((uint4*)a, (int64_t)(abytes / 16), (uint4*)b,
                                             (int64_t)(bbytes / 16), (uint4*)c,
                                             (int64_t)(cbytes / 16), keep_a);

@@ -1028,7 +1028,7 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   const int A = d.nx > d.ny ? d.nx : d.ny, B = A;
   const int K = lp.neg_cells;
   // tiles: about one block per SM over the 4 cones, at least 8 lines each
-  int T = (4 * A + 147) / 148;
+  int T = (4 * A + d.sms - 1) / d.sms;
   T = T < 8 ? 8 : ((T + 7) / 8) * 8;
 #ifdef GVOM_NEG_T
   T = GVOM_NEG_T;
@@ -1081,7 +1081,7 @@ cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPt
   // 32 x 32 tiles (1024 threads) when they give at least two blocks per SM,
   // else 16 x 16 (more blocks for small maps, more halo per cell)
   const int64_t t32 = ((d.nx + 31) / 32) * (int64_t)((d.ny + 31) / 32);
-  const int tile = t32 >= 2 * 148 ? 32 : 16;
+  const int tile = t32 >= 2 * (int64_t)d.sms ? 32 : 16;
   const size_t smem = neg8_smem_bytes(lp.neg_cells, tile);
   if (smem > kNegSmemMax) return cudaErrorInvalidConfiguration;
   const dim3 grid((unsigned)((d.nx + tile - 1) / tile), (unsigned)((d.ny + tile - 1) / tile));

@@ -8,39 +8,18 @@
 // over the slab's tiles) and accumulates the per-return statistics
 // (k_endpoint_records).  After the surface rows are all-gathered,
 // k_transpose_init prepares the cone sweeps over the whole map.
-#include "gvom_internal.cuh"
+#include "gvom_device.cuh"
 
 namespace gvom {
 
 namespace {
-
-constexpr float kGLim = 4194304.0f;  // |g_i| < 2^22 voxels (reading A5)
-
-// O3 (same float order as k_integrate.cu's transform_point)
-__device__ __forceinline__ bool xform(const SensorParams& sp, const float4 p, float& g0, float& g1,
-                                      float& g2) {
-  if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) return false;
-  if (p.x == 0.0f && p.y == 0.0f && p.z == 0.0f) return false;
-  float g[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const float t0 = __fmul_rn(sp.A[3 * i + 0], p.x);
-    const float t1 = __fmul_rn(sp.A[3 * i + 1], p.y);
-    const float t2 = __fmul_rn(sp.A[3 * i + 2], p.z);
-    g[i] = __fadd_rn(__fadd_rn(__fadd_rn(t0, t1), t2), sp.b[i]);
-  }
-  g0 = g[0];
-  g1 = g[1];
-  g2 = g[2];
-  return fabsf(g0) < kGLim && fabsf(g1) < kGLim && fabsf(g2) < kGLim;
-}
 
 // in-grid return -> record + destination slab (by row y); false otherwise
 __device__ __forceinline__ bool return_record(const SensorParams& sp, const float4 q,
                                               const Dims& d, const SlabBounds& sb, EpRecord& r,
                                               int& dest) {
   float g0, g1, g2;
-  if (!xform(sp, q, g0, g1, g2)) return false;
+  if (!transform_point(sp, q, g0, g1, g2)) return false;
   const int e0 = (int)floorf(g0), e1 = (int)floorf(g1), e2 = (int)floorf(g2);
   if ((unsigned)e0 >= (unsigned)d.nx || (unsigned)e1 >= (unsigned)d.ny ||
       (unsigned)e2 >= (unsigned)d.nz)
@@ -108,14 +87,6 @@ __global__ void __launch_bounds__(256) k_slab_bits(const EpRecord* __restrict__ 
     atomicAdd(tile_counts + tile, (uint32_t)__popc(peers));
 }
 
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
-}
 
 // exclusive offsets of the tile counts in [t0, t1) (relative to t0) and their
 // total -> *tc.total; one block, each thread a contiguous chunk

@@ -27,7 +27,7 @@ LAYER_ID = {"height": 0, "density": 1, "hard": 2, "soft": 3, "neg": 4, "slope": 
             "spread": 7}
 LAYER_U8 = {"hard", "soft", "neg"}
 STAGES = ("raycast", "rank_count", "rank_scan", "finalize", "endpoint", "columns", "slope",
-          "negative", "memset", "h2d", "export", "merge")
+          "negative", "memset", "h2d", "export", "merge", "integrate", "maps")
 STATUS = {0: "ok", -1: "invalid argument", -2: "workspace too small", -3: "CUDA error",
           -4: "sensor outside the map", -5: "empty map buffer", -6: "capacity too small"}
 
@@ -95,6 +95,7 @@ def load_library() -> C.CDLL:
         "gvom_export_layers_cost": ([P, P, P, P, P, C.c_size_t], I32),
         "gvom_export_window": ([P, P, P, P, P, P], I32),
         "gvom_graph_stats": ([P, P], I32),
+        "gvom_debug_inject_fault": ([P, I32], I32),
         "gvom_map_origin": ([P, P], I32),
         "gvom_export_voxels": ([P, P, P, I64, P], I32),
         "gvom_export_frame": ([P, I32, P, P, I64, P, P], I32),
@@ -131,7 +132,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
             "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers",
-            "gvom_obstacle_buffers")
+            "gvom_obstacle_buffers", "gvom_debug_inject_fault")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -216,6 +217,16 @@ class GvomMap:
         _check(self.lib.gvom_synchronize(self.h), "gvom_synchronize")
         self._keep.clear()
 
+    def _retain(self, keep):
+        """Keep a call's input tensors alive until the handle's stream passes
+        the call: an event is recorded after it, and entries whose event has
+        completed are dropped on every call (bounded, with no host sync)."""
+        self._keep = [(ev, k) for ev, k in self._keep if not ev.query()]
+        if keep:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            self._keep.append((ev, keep))
+
     # -- the five calls ------------------------------------------------------
     def shift(self, vehicle_xyz: Sequence[float]) -> np.ndarray:
         p = (C.c_double * 3)(*[float(v) for v in vehicle_xyz])
@@ -256,6 +267,7 @@ class GvomMap:
         _check(self.lib.gvom_partial_scan(self.h, arr, n, C.c_void_p(miss.data_ptr()),
                                           C.c_void_p(records.data_ptr()), records.numel(), ys, P,
                                           cnt), "gvom_partial_scan")
+        self._retain(keep)
         return [int(c) for c in cnt]
 
     def slab_occupancy(self, y0: int, y1: int, records: torch.Tensor, n: int) -> int:
@@ -326,7 +338,7 @@ class GvomMap:
         """(hard, soft): uint8 [ny, nx] views of the library's obstacle layers."""
         hp, sp_ = C.c_void_p(), C.c_void_p()
         _check(self.lib.gvom_obstacle_buffers(self.h, C.byref(hp), C.byref(sp_)),
-               "gvom_obstacle_buffers")
+               "gvom_obstacle_buffers", "gvom_debug_inject_fault")
         n = self.nx * self.ny
         views = []
         for ptr in (hp, sp_):
@@ -341,7 +353,7 @@ class GvomMap:
         arr, n, keep = self._scan_array(scans)
         rc = self.lib.gvom_integrate_scan(self.h, arr, n)
         _check(rc, "gvom_integrate_scan")
-        self._keep.append(keep)  # host buffers must live until the stream passes
+        self._retain(keep)  # input buffers must live until the stream passes
 
     def compute_maps(self):
         _check(self.lib.gvom_compute_maps(self.h), "gvom_compute_maps")
@@ -408,7 +420,7 @@ class GvomMap:
             w, cost = self._cost_dst(cost_weights, cost)
             cp, cb = C.c_void_p(cost.data_ptr()), cost.numel() * 4
         _check(self.lib.gvom_step(self.h, p, arr, n, ptrs, sizes, w, cp, cb, dlt), "gvom_step")
-        self._keep.append(keep)
+        self._retain(keep)
         if cost_weights is not None:
             res = {} if res is None else res
             res["cost"] = cost
@@ -432,6 +444,10 @@ class GvomMap:
         o = (C.c_int64 * 3)()
         _check(self.lib.gvom_graph_stats(self.h, o), "gvom_graph_stats")
         return {"graph_launches": o[0], "instantiations": o[1], "eager_steps": o[2]}
+
+    def inject_fault(self, what: int = 1):
+        """Test hook: 1 = the next gvom_step capture fails (GVOM_FAULT_CAPTURE)."""
+        _check(self.lib.gvom_debug_inject_fault(self.h, int(what)), "gvom_debug_inject_fault")
 
     def costmap(self, weights, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """Weighted per-pixel sum of the layers; weights = (hard, soft,

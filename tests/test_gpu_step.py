@@ -156,3 +156,31 @@ def test_pipelined_step_graphs_overlap_frames():
         compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
     st = m.graph_stats()
     assert st["graph_launches"] == len(w.frames), st
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_step_capture_failure_rolls_back(pipeline):
+    # a failed capture must not leave the ring naming a slot whose
+    # frame never ran.  Frame 1's step fails (injected capture fault): the
+    # state is as if it had never been called, so after frames 0 and 2 the
+    # map equals the oracle's with frames 0 and 2 only (its shift stands).
+    w = synth.config3(speed=12.0, n_frames=3, columns=1024)
+    if pipeline:
+        w.grid["pipeline"] = True
+    m = GvomMap(w.grid, max_points_per_frame=w.points_per_frame)
+    om = O.OracleMap(w.grid)
+    for i, f in enumerate(w.frames):
+        scans = [to_dev(s) for s in f.scans]
+        if i == 1:
+            m.inject_fault(1)
+            with pytest.raises(Exception):
+                m.step(f.vehicle_xyz, scans, export=False)
+            om.shift(f.vehicle_xyz)
+            continue
+        m.step(f.vehicle_xyz, scans, export=False)
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in f.scans])
+    compare_layers(layers_np(m), om.compute_maps())
+    lut, data, origin = m.export_frame(1)
+    assert np.array_equal(origin, om.buffer[-2].origin)
+    assert np.array_equal(lut, om.buffer[-2].lut)
