@@ -20,9 +20,18 @@ roofline = the dominant kernel (ray cast): algorithmic bytes per launch
          duration, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the oracle (oracle/, single-threaded C) on the same workload.
 
+partitioned = (N = 1) the partitioned path of N > 1 on one rank: BASELINE
+         configs[4] (8 streams, 4.2M points, 1024x1024x128) through the slab
+         calls -- the N = 1 point of the strong-scaling curve.
+
 --impl reference runs the oracle as the reference arm (CPU; rank 0 only).
-N > 1 (torchrun): every rank runs its own frame stream (independent maps, no
-data-path collective; weak scaling); time = max over ranks.
+N > 1 (torchrun): the partitioned path on BASELINE configs[4]:
+the sensors of ONE frame sharded over the ranks; by default (--slab-mode
+segments) their points are all-gathered and each rank traces the ray segments
+inside its own y-slab (gvom_integrate_slab); --slab-mode reduce_scatter /
+fused runs the dense miss-grid reduce-scatter (NCCL) / its symmetric-memory
+fused finalize.  Strong scaling, time = max over ranks.  --replicas instead
+runs independent per-GPU frame streams (weak scaling, no collective).
 """
 from __future__ import annotations
 
@@ -52,19 +61,28 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gvom", choices=["gvom", "reference"])
-    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE.json configs index (default: 1 = c2; with N > 1 the "
+                         "partitioned path on 4 = c5)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent per-GPU frame streams instead of the "
+                         "partitioned path")
+    ap.add_argument("--no-partitioned", action="store_true",
+                    help="N = 1: skip the partitioned-path reference line (c5, one rank)")
     ap.add_argument("--frames", type=int, default=4, help="distinct scans cycled")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--neg8cone", action="store_true",
                     help="GVOM_FLAG_NEG_8CONE variant (8-cone negative-obstacle search)")
-    ap.add_argument("--fused", action="store_true",
-                    help="slab path: miss grids in symmetric memory, summed by the slab "
-                         "finalize over peer memory (gvom_slab_finalize_peers)")
+    ap.add_argument("--slab-mode", default="segments",
+                    choices=["segments", "reduce_scatter", "fused"],
+                    help="partitioned path: ray segments per slab (default), the dense "
+                         "miss-grid reduce-scatter, or its fused symmetric-memory variant "
+                         "(gvom_slab_finalize_peers)")
     ap.add_argument("--rolling", action="store_true",
                     help="GVOM_FLAG_ROLLING variant (one accumulated window map, K = inf)")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work")
     ap.add_argument("--slab", action="store_true",
-                    help="multi-GPU slab partition of one frame (default for --config 4, N > 1)")
+                    help="the partitioned path (slab partition of one frame) at any N")
     return ap.parse_args()
 
 
@@ -109,6 +127,53 @@ def measured_traffic(workload: str):
                 (float(inst) if inst is not None else None))
     except Exception:
         return None, None, None
+
+
+def l2_red_ceiling():
+    """the L2 reduction ceiling of the ray cast's miss counting --
+    red.global.add.u32 into 16 / 64 / 512 MB arrays (tools library
+    libgvom_probe.so, csrc/probe/l2_red_probe.cu).  Per size: random words
+    (one L2 request per lane), one 128-byte line per warp instruction (32
+    atomic ops per request), and runs of 4 lanes (one red per run, the merged
+    shape of the ray cast's steps)."""
+    import ctypes as C
+    from paper_2109_13176_b200 import build_ext
+    try:
+        lib = C.CDLL(build_ext.PROBE_LIB)
+    except OSError as e:
+        return {"error": str(e)}
+    lib.probe_red.argtypes = [C.c_int64, C.c_int, C.c_int64, C.POINTER(C.c_float),
+                              C.POINTER(C.c_int64)]
+    lib.probe_red.restype = C.c_int
+    out = {}
+    n_warp_iters = 1 << 20
+    for mb in (16, 64, 512):
+        row = {}
+        for pat, name, lanes in ((0, "random_word", 32), (1, "line_per_warp", 32),
+                                 (2, "runs_of_4", 8)):
+            ms = C.c_float(0.0)
+            ninst = C.c_int64(0)
+            rc = lib.probe_red(mb << 20, pat, n_warp_iters, C.byref(ms), C.byref(ninst))
+            if rc < 0 or ms.value <= 0:
+                row[name] = None
+                continue
+            inst = ninst.value
+            reqs = inst * (32 if pat == 0 else (1 if pat == 1 else 8))
+            row[name] = {"g_red_lanes_s": inst * lanes / (ms.value / 1e3) / 1e9,
+                         "g_l2_requests_s": reqs / (ms.value / 1e3) / 1e9,
+                         "ms": ms.value}
+        out[f"{mb}MB"] = row
+    return out
+
+
+def measured_red_requests(workload: str):
+    """L2 reduction requests per k_raycast launch (committed ncu capture)."""
+    p = os.path.join(ROOT, "profiles", "raycast_traffic.json")
+    try:
+        v = json.load(open(p)).get("red_requests_per_launch", {}).get(workload)
+        return None if v is None else float(v)
+    except Exception:
+        return None
 
 
 # issue peak: 148 SMs x 4 schedulers x one warp instruction per cycle at the
@@ -239,6 +304,8 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    if args.config is None:  # the config our arm runs at this N
+        args.config = 4 if (world > 1 and not args.replicas) else 1
     w = load_workload(args.config, args.frames, 0)
     budget = float(os.environ.get("GVOM_REF_BUDGET_S", "60"))
     # warmup: one untimed update; then timed updates bounded by the budget
@@ -266,20 +333,40 @@ def run_reference(args):
     return 0
 
 
-def main_slab(args):
+def ensure_dist(dev):
+    """torch.distributed for the slab path; a single process (plain `python
+    bench.py`) gets a one-rank group on 127.0.0.1."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        return
+    if "RANK" not in os.environ:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+                          WORLD_SIZE="1", LOCAL_RANK="0")
+    dist.init_process_group("nccl", device_id=dev)
+
+
+def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int = 1):
     """the points of ONE frame are sharded across the ranks (sensor
-    i -> rank i % N); miss grids are reduce-scattered by y-slab over NCCL,
-    returns routed to slab owners, surface rows all-gathered.  Strong scaling:
-    value = points of the whole frame per second (max-over-ranks time)."""
+    i -> rank i % N).  mode "segments": the points are all-gathered and each
+    rank traces only the ray segments inside its y-slab; "reduce_scatter":
+    dense partial miss grids reduce-scattered by y-slab over NCCL, returns
+    routed to slab owners; "fused": those grids summed by the slab finalize
+    over symmetric peer memory.  Surface rows all-gathered in every mode.
+    Strong scaling: value = points of the whole frame per second, time = max
+    over ranks.  Returns the JSON line (rank 0) or None."""
     import torch
     import torch.distributed as dist
 
     from paper_2109_13176_b200 import GvomMap, parallel
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    w = load_workload(args.config, args.frames, 0)  # the same frame on every rank
+    ensure_dist(dev)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    w = load_workload(cfg_index, frames, 0)  # the same frame on every rank
     f = w.frames[0]
     grid = dict(w.grid)
     grid["buffer_frames"] = 1
@@ -289,7 +376,10 @@ def main_slab(args):
     stream = torch.cuda.Stream(device=dev)
     # capacity for the whole frame: data rows sit at their global ranks
     m = GvomMap(grid, max_points_per_frame=max(1, npts_all), device=dev, stream=stream)
-    sm = parallel.SlabMapper(m, ep_capacity=npts_all, fused=args.fused)
+    if mode == "segments":
+        sm = parallel.SegmentMapper(m)
+    else:
+        sm = parallel.SlabMapper(m, ep_capacity=npts_all, fused=(mode == "fused"))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step():
@@ -298,13 +388,13 @@ def main_slab(args):
         sm.compute_maps()
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             step()
         torch.cuda.synchronize()
         dist.barrier()
         total = 0.0
         with ClockSampler(local) as clk:
-            for _ in range(args.steps):
+            for _ in range(steps):
                 flush.zero_()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -316,22 +406,37 @@ def main_slab(args):
     t = torch.tensor([total], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t[0])
+    line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": npts_all * args.steps / (total / 1e3), "unit": "points/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "strong",
+            "metric": METRIC, "value": npts_all * steps / (total / 1e3), "unit": "points/s",
+            "n_gpus": world, "steps": steps, "warmup": warmup,
+            "ms_per_step": total / steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
             "config": {"workload": w.name, "points_per_frame": npts_all, "sensors": len(f.scans),
                        "grid": f"{m.nx}x{m.ny}x{m.nz}@{w.grid['res']}m", "buffer_frames": 1,
-                       "parallelism": f"slab{world}: sensors sharded, " + (
-                           "miss grids summed over peer memory in the slab finalize"
-                           if args.fused else "reduce-scatter by y-slab"),
+                       "parallelism": f"slab{world}: sensors sharded, " + {
+                           "segments": "points all-gathered, each rank traces the ray "
+                                       "segments inside its rows (gvom_integrate_slab)",
+                           "fused": "miss grids summed over peer memory in the slab finalize",
+                           "reduce_scatter": "reduce-scatter of the miss grids by y-slab"}[mode],
                        "l2": "flushed (256 MiB write) between steps",
                        "step": "shift+partial_scan+exchange+slab_finalize+slab maps"},
-            "map_updates_per_s": args.steps / (total / 1e3),
+            "map_updates_per_s": steps / (total / 1e3),
             "gpu_launches": None, "clocks": clk.summary(),
         }
+    del sm, m
+    dist.barrier()
+    return line
+
+
+def main_slab(args):
+    """The partitioned path as the bench line (N > 1 by default: BASELINE
+    configs[4], the multi-GPU workload; --config chooses another)."""
+    import torch.distributed as dist
+    cfg = 4 if args.config is None else args.config
+    line = slab_measure(cfg, args.steps, args.warmup, args.slab_mode)
+    if line is not None:
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
@@ -404,8 +509,11 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    if args.slab or (args.config == 4 and world > 1):
+    # N > 1: the partitioned path unless --replicas
+    if args.slab or (world > 1 and not args.replicas):
         return main_slab(args)
+    if args.config is None:
+        args.config = 1  # BASELINE metric config (c2)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
     torch.cuda.set_device(local)
@@ -454,15 +562,15 @@ def main():
         torch.cuda.synchronize()
 
     with torch.cuda.stream(stream):
-        # only the dominant kernel is bracketed by events (roofline); the
-        # per-stage breakdown comes from a separate instrumented pass below.
-        # Timing is on from the warm-up so that the step graph's topology (its
-        # event nodes) is instantiated before the timed region.
-        m.set_timing(True, stages=["raycast", "integrate", "maps"])
+        # The timed region runs the step graph with no event nodes inside it
+        # (event-record nodes between a graph's kernels cost several us per
+        # step).  The dominant kernel's launch time (roofline) and the whole
+        # integrate / compute_maps calls are timed in a second pass of graphed
+        # steps with events around them; the per-launch breakdown comes from a
+        # third, instrumented pass of separate calls.
         for i in range(args.warmup):
             step(i, dev_frames[i % len(frames)], out)
         stream.synchronize()
-        m.stage_times()  # clear
         # ---- timed region: device-resident inputs --------------------------
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
@@ -477,8 +585,19 @@ def main():
             stream.synchronize()
         barrier()
         launches = m.launch_count() - launches0
-        stage = m.stage_times()
         gstats = m.graph_stats()
+        # kernel pass: graphed steps with events around the ray cast and
+        # around the integrate / compute_maps calls
+        m.set_timing(True, stages=["raycast", "integrate", "maps"])
+        for i in range(3):
+            step(i, dev_frames[i % len(frames)], out)
+        stream.synchronize()
+        m.stage_times()  # clear
+        for i in range(args.steps):
+            flush.zero_()
+            step(i, dev_frames[i % len(frames)], out)
+        stage = m.stage_times()
+        m.set_timing(False)
         # instrumented pass (not timed): every stage bracketed by events
         m.set_timing(True)
         n_inst = min(args.steps, 50)
@@ -554,6 +673,8 @@ def main():
     K = int(w.grid["buffer_frames"])
     maps_ms = stage["maps"][0] / max(stage["maps"][1], 1)
 
+    l2_red = l2_red_ceiling() if rank == 0 else None
+    red_req = measured_red_requests(w.name)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -583,14 +704,23 @@ def main():
                              "note": "the kernel's actual limiter: warp instructions (ncu, "
                                      "committed capture) / live launch time vs the SM issue "
                                      "peak; its miss RMWs are L2-resident at this size"},
-                         "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)"},
+                         "bytes_model": "16 N + 8 M + 8 H (points, miss RMW, endpoint bit RMW)",
+                         "l2_red": l2_red,
+                         "raycast_red": {
+                             "g_increments_s": Mi / launches_per_frame / (ray_launch_ms / 1e3) / 1e9,
+                             "g_l2_requests_s": (None if red_req is None else
+                                                 red_req / (ray_launch_ms / 1e3) / 1e9),
+                             "note": "miss increments (M per launch) and L2 reduction requests "
+                                     "per launch (ncu lts__t_requests_srcunit_tex_op_red, "
+                                     "committed capture) over the live launch time; compare "
+                                     "l2_red (the probe's ceiling at the miss grid's size)"}},
             "integrate": {"ms_per_frame": integ_ms, "points_per_s": npts / (integ_ms / 1e3),
                           "B_int_bytes": B_int, "hbm_frac": B_int / (integ_ms / 1e3) / 1e9 / peak,
                           "H": H, "M": Mi, "k": k,
-                          "timing": "events around gvom_integrate_scan inside the timed graphed "
-                                    "steps (GVOM_STAGE_INTEGRATE)"},
+                          "timing": "events around gvom_integrate_scan in a second pass of graphed "
+                                    "steps (GVOM_STAGE_INTEGRATE), L2 flushed between steps"},
             "compute_maps_ms": maps_ms,
-            "compute_maps_timing": "events around gvom_compute_maps inside the timed graphed "
+            "compute_maps_timing": "events around gvom_compute_maps in a second pass of graphed "
                                    "steps (GVOM_STAGE_MAPS)",
             "stages_ms_per_step": {s: v[0] / n_inst for s, v in stage_all.items() if v[1]},
             "stages_note": "separate instrumented pass (events around every launch, "
@@ -619,8 +749,17 @@ def main():
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+    if world == 1 and not args.no_partitioned:
+        # the partitioned path (what N > 1 runs) at one rank: the N = 1 point of
+        # its strong-scaling curve
+        part = slab_measure(4, min(args.steps, 20), 3, args.slab_mode)
+        if rank == 0:
+            part["note"] = ("BASELINE configs[4] through the slab-partition path on one rank "
+                            "(the N = 1 point of `bench.py --gpus N`, N > 1)")
+            line["partitioned"] = part
+    if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     return 0

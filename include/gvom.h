@@ -184,6 +184,24 @@ GVOM_API gvom_status gvom_shift(gvom_handle* h, const double vehicle_xyz[3], int
  * rejected, state unchanged).  n_scans = 0 pushes an empty map.    */
 GVOM_API gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans);
 
+/* The ray-segment slab partition (multi-GPU, DESIGN.md
+ * section 8): gvom_integrate_scan restricted to the map rows [y0, y1) that
+ * this rank owns.  scans are ALL sensors of the frame (every rank sees every
+ * ray); each ray is traced only over the steps whose voxel lies in the rows
+ * (y is monotone along a ray, so that is one step range, entered at its exact
+ * walk state through the stateless keys of O5), and only returns in the rows
+ * are binned.  The buffer map pushed holds the slab's voxels with LOCAL data
+ * ranks (0..k_slab-1, in L order; the frame's global rank of a voxel = the k
+ * of the slabs before + its local rank); voxels outside the rows are not
+ * defined.  Every pass-through and return of the frame is counted by exactly
+ * one rank, so the union of the slabs equals gvom_integrate_scan's map.  No
+ * collective is needed for the map: the compute_maps_slab phases follow.
+ * Not with GVOM_FLAG_PIPELINE or GVOM_FLAG_ROLLING; buffer_frames = 1 (a
+ * shifted older map would read rows of other slabs).  Errors as
+ * gvom_integrate_scan, GVOM_E_INVALID for a bad row range.               */
+GVOM_API gvom_status gvom_integrate_slab(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                         int32_t y0, int32_t y1);
+
 /* Map processing: combine all buffer maps at the origin of the
  * newest one, then compute height, density, hard, soft, slope,
  * roughness and negative-obstacle layers.  GVOM_E_EMPTY if no map.         */
@@ -300,7 +318,10 @@ GVOM_API gvom_status gvom_export_frame(gvom_handle* h, int32_t age, int32_t* d_l
  *     the q_s rows into gvom_surface_buffer() (and, with
  *     GVOM_FLAG_SLOPE_SKIP_OBSTACLES, of the hard / soft rows into
  *     gvom_obstacle_buffers()); phase 1: slope, roughness and negative
- *     obstacles for the whole map from the gathered surface.
+ *     obstacles of the slab rows [y0, y1) from the gathered surface (their
+ *     windows and cones read the rows around the slab; with
+ *     GVOM_FLAG_NEG_8CONE the 8-cone search still covers the whole map).
+ *     Layers are defined on the slab rows only.
  * Sums and mins are exact integers, so the result is identical to one GPU.  */
 typedef struct gvom_endpoint {
   uint32_t L;  /* linear voxel index of an in-grid return          */

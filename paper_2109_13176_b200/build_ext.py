@@ -67,5 +67,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+PROBE_SRC = os.path.join(CSRC, "probe", "l2_red_probe.cu")
+PROBE_LIB = os.path.join(LIBDIR, "libgvom_probe.so")
+
+
+def build_probe(force: bool = False) -> str:
+    """The L2-reduction microbenchmark (a measurement tool for bench.py's
+    roofline, not part of the gvom ABI)."""
+    if not force and os.path.exists(PROBE_LIB) and \
+            os.path.getmtime(PROBE_LIB) >= os.path.getmtime(PROBE_SRC):
+        return PROBE_LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = PROBE_LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([nvcc(), *NVCC_FLAGS, "-shared", "-cudart", "static", PROBE_SRC,
+                           "-o", tmp])
+    os.replace(tmp, PROBE_LIB)
+    return PROBE_LIB
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -60,7 +60,8 @@ bool valid_config(const gvom_config* c) {
   if (!(c->res > 0) || !isfinite(c->res)) return false;
   if (!(c->z_center_frac >= 0.0 && c->z_center_frac <= 1.0)) return false;
   if (c->buffer_frames < 1 || c->buffer_frames > GVOM_MAX_BUFFER_FRAMES) return false;
-  if (c->max_points_per_frame < 0) return false;
+  // LUT-direct miss counting: N_m <= points per frame <= 2^30 (A11's cap never binds)
+  if (c->max_points_per_frame < 0 || c->max_points_per_frame > (1ll << 30)) return false;
   if (!(c->min_obstacle_height >= 0) || !(c->max_obstacle_height >= c->min_obstacle_height))
     return false;
   if (!(c->density_threshold >= 0.0 && c->density_threshold <= 1.0)) return false;
@@ -578,6 +579,8 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
   h->lp.neg_qb = neg_qbits(cfg->nz);
   h->lp.skip_obstacles = (cfg->flags & GVOM_FLAG_SLOPE_SKIP_OBSTACLES) ? 1 : 0;
   h->lp.neg_8cone = (cfg->flags & GVOM_FLAG_NEG_8CONE) ? 1 : 0;
+  h->lp.row0 = 0;
+  h->lp.row1 = cfg->ny;
   const double zero[3] = {0, 0, 0};
   snap(*cfg, zero, h->origin);
   h->rolling = (cfg->flags & GVOM_FLAG_ROLLING) != 0;
@@ -759,18 +762,22 @@ static std::vector<RayBatch> ray_batches(const gvom_scan* scans, int32_t n_scans
 }
 
 static cudaError_t raycast_frame(gvom_handle* h, const std::vector<RayBatch>& batches,
-                                 uint32_t* miss, uint32_t* bits, const TileCounts& tc) {
+                                 uint32_t* miss, uint32_t* bits, const TileCounts& tc,
+                                 const SlabRange* slab = nullptr, bool lut_direct = false) {
   for (size_t k = 0; k < batches.size(); ++k) {
     const cudaError_t e = stage(h, GVOM_STAGE_RAYCAST, true, [&] {
-      return launch_raycast(batches[k], h->d, miss, bits, tc, k + 1 == batches.size(), h->st);
+      return launch_raycast(batches[k], h->d, miss, bits, tc, k + 1 == batches.size(), h->st,
+                            slab, lut_direct);
     });
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
-  NvtxRange nvtx_("gvom_integrate_scan");
+// integrate_scan over the rows [slab.y0, slab.y1) (the whole map, or a rank's
+// slab in the ray-segment partition)
+static gvom_status integrate_rows(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                  const SlabRange& slab) {
   SensorParams sp[GVOM_MAX_SENSORS];
   const gvom_status ps = prepare_scans(h, scans, n_scans, sp);
   if (ps != GVOM_OK) return ps;
@@ -778,12 +785,12 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
   const Dims& d = h->d;
   GVOM_CU(wait_slot_readers(h, h->head));
   Bracket br(h, GVOM_STAGE_INTEGRATE, h->st);
-  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true, [&] {
-    return launch_zero3(slot.lut, (size_t)h->lay.slot_bits, slot.bits,
-                        (size_t)(h->lay.slot_wprefix - h->lay.slot_bits), h->tc.tile,
-                        h->lay.tilecnt_bytes, h->d, h->st);
-  }));
-  // pass 2a: ray tracing into the slot's LUT buffer (used as a u32 miss grid)
+  int64_t t0, t1;  // the tiles of the rows integrated
+  slab_tile_range(d, slab, &t0, &t1);
+  // pass 0: the slot's LUT to -1 (empty, no misses), its bits cleared
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true,
+                [&] { return launch_reset_slot(slot.lut, slot.bits, d, t0, t1, h->st); }));
+  // pass 2a: ray tracing, misses counted down in the slot's LUT (LUT-direct)
   TileCounts tc = h->tc;
   tc.total = slot.meta;
   std::vector<const float4*> dptr;
@@ -792,15 +799,22 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     if (st != GVOM_OK) return st;
   }
   const std::vector<RayBatch> batches = ray_batches(scans, n_scans, dptr, sp);
-  GVOM_CU(raycast_frame(h, batches, (uint32_t*)slot.lut, slot.bits, tc));
-  // pass 1: occupied-voxel ranks (deterministic, L order) -> LUT + data rows
+  const bool part = slab.y0 > 0 || slab.y1 < h->cfg.ny;
+  GVOM_CU(raycast_frame(h, batches, (uint32_t*)slot.lut, slot.bits, tc, part ? &slab : nullptr,
+                        true));
+  if (batches.empty())  // no ray-cast launch scanned the (all zero) tile counts
+    GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+      return cudaMemsetAsync(tc.offset, 0, 4 * (size_t)n_tiles(d), h->st);
+    }));
+  // pass 1: ranks of the occupied voxels in L order -> LUT entries + data rows
   GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
-    return launch_finalize_tiles(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, h->st);
+    return launch_finalize_lut(slot.lut, slot.bits, slot.wprefix, slot.data, tc, d, t0, t1,
+                               h->st);
   }));
   // pass 2b: per-return metrics into the data rows, one launch per batch
   for (const RayBatch& b : batches)
     GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true,
-                  [&] { return launch_endpoint(b, d, slot.lut, slot.data, h->st); }));
+                  [&] { return launch_endpoint(b, d, slot.lut, slot.data, h->st, slab); }));
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
   if (h->rolling)  // the frame map joins the window map (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
@@ -813,6 +827,20 @@ gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t 
     GVOM_CU(cudaEventRecordWithFlags(h->ev_integrated, h->st,
                                      h->capturing ? cudaEventRecordExternal : 0u));
   return GVOM_OK;
+}
+
+gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans, int32_t n_scans) {
+  NvtxRange nvtx_("gvom_integrate_scan");
+  if (!h) return GVOM_E_INVALID;
+  return integrate_rows(h, scans, n_scans, SlabRange{0, h->cfg.ny});
+}
+
+gvom_status gvom_integrate_slab(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
+                                int32_t y0, int32_t y1) {
+  NvtxRange nvtx_("gvom_integrate_slab");
+  if (!h || h->pipelined || h->rolling || y0 < 0 || y1 > h->cfg.ny || y0 >= y1)
+    return GVOM_E_INVALID;
+  return integrate_rows(h, scans, n_scans, SlabRange{y0, y1});
 }
 
 // Layers from the surface: the cone search (+ Delta-H decision) on the aux
@@ -848,6 +876,8 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
     GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_integrated,
                                 h->capturing ? cudaEventWaitExternal : 0u));
   h->lp.o_z = o[2];
+  h->lp.row0 = 0;  // every row
+  h->lp.row1 = h->cfg.ny;
   Bracket br(h, GVOM_STAGE_MAPS, h->ms());
   if (h->rolling) {  // the window map at the current origin (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true,
@@ -1267,6 +1297,10 @@ static gvom_status slab_finalize(gvom_handle* h, int32_t y0, int32_t y1,
   GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true, [&] {
     return launch_endpoint_records((const EpRecord*)d_ep, n_ep, slot.lut, slot.data, h->st);
   }));
+  // the integrate path expects zero tile counters at rest
+  GVOM_CU(stage(h, GVOM_STAGE_MEMSET, false, [&] {
+    return cudaMemsetAsync(h->tc.tile, 0, h->lay.tilecnt_bytes, h->st);
+  }));
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
   h->head = (h->head + 1) % h->NS;
   if (h->count < h->K) h->count++;
@@ -1336,6 +1370,10 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
   }
   GVOM_CU(stage(h, GVOM_STAGE_NEGATIVE, true,
                 [&] { return launch_transpose_init(h->d, h->lp, h->layers, h->st); }));
+  // slope / roughness / negative obstacles of the slab's rows only (their
+  // windows and cones read the gathered surface rows around them)
+  h->lp.row0 = y0;
+  h->lp.row1 = y1;
   GVOM_CU(surface_layers(h));
   h->maps_valid = true;
   return GVOM_OK;

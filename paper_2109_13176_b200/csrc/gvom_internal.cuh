@@ -78,6 +78,9 @@ struct LayerParams {
   int32_t skip_obstacles;  // GVOM_FLAG_SLOPE_SKIP_OBSTACLES
   int32_t neg_8cone;       // GVOM_FLAG_NEG_8CONE
   int32_t neg_qb;          // q_s < 2^neg_qb (= 16 + ceil(log2 nz)); see neg_keys
+  // rows [row0, row1) whose slope / roughness / negative-obstacle cells are
+  // computed (the whole map, or a rank's slab in phase 1 of the slab path)
+  int32_t row0, row1;
 };
 
 // Cone-sweep keys (k_negative): a found ring (distance D, heights q) is packed
@@ -145,9 +148,16 @@ struct RayBatch {
   int64_t n[kRayBatch];
   SensorParams sp[kRayBatch];
 };
+// Rows [y0, y1) of the map a rank owns (the ray-segment slab partition): the
+// ray cast traces only the part of every ray inside them, and only returns
+// inside them are binned.  {0, ny} = the whole map.
+struct SlabRange {
+  int32_t y0, y1;
+};
 cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_grid,
                            uint32_t* bits, const TileCounts& tc, bool last_launch,
-                           cudaStream_t st);
+                           cudaStream_t st, const SlabRange* slab = nullptr,
+                           bool lut_direct = false);
 // rank (from the tile counts) + in-place LUT encode + data-row init, one launch
 // the P ranks' partial miss grids, device pointers the GPU can load from
 // (peer memory, NEXT-2): the finalize sums them instead of reading lut_inplace
@@ -160,6 +170,20 @@ cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, ui
                                   gvom_voxel* data, const TileCounts& tc, const Dims& d,
                                   cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1,
                                   uint32_t base = 0, const PeerGrids* peers = nullptr);
+// the integrate path (LUT-direct): pass 0 resets the slot's LUT tiles [t0, t1)
+// to -1 and clears their bits; the ray cast counts misses down in place; pass 1
+// ranks the occupied voxels and initialises their rows (k_finalize_lut)
+cudaError_t launch_reset_slot(int32_t* lut, uint32_t* bits, const Dims& d, int64_t t0,
+                              int64_t t1, cudaStream_t st);
+cudaError_t launch_finalize_lut(int32_t* lut, const uint32_t* bits, uint32_t* wprefix,
+                                gvom_voxel* data, const TileCounts& tc, const Dims& d, int64_t t0,
+                                int64_t t1, cudaStream_t st);
+// tiles [*t0, *t1) holding the voxels of rows [y0, y1)
+inline void slab_tile_range(const Dims& d, const SlabRange& s, int64_t* t0, int64_t* t1) {
+  const int64_t row = (int64_t)d.nx * d.nz;
+  *t0 = ((int64_t)s.y0 * row) >> kTileShift;
+  *t1 = (((int64_t)s.y1 * row) + (1 << kTileShift) - 1) >> kTileShift;
+}
 cudaError_t launch_rank(const uint32_t* bits, const Dims& d, uint32_t* wprefix, uint64_t* status,
                         unsigned long long* ticket, uint64_t base, uint32_t epoch,
                         uint32_t* total, cudaStream_t st);
@@ -168,7 +192,7 @@ cudaError_t launch_zero3(void* a, size_t abytes, void* b, size_t bbytes, void* c
                          const Dims& d, cudaStream_t st);
 // per-return hits / min_dz / moments of a sensor batch (same tiling as the ray cast)
 cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lut,
-                            gvom_voxel* data, cudaStream_t st);
+                            gvom_voxel* data, cudaStream_t st, const SlabRange& slab);
 cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                              cudaStream_t st);  // 8-cone variant -> neg directly
 cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& lp,

@@ -41,7 +41,8 @@ __device__ __forceinline__ int64_t point_index(int64_t tid, int32_t rings) {
 // astronomically rare rays whose reciprocal 1/d_a is not finite, where the
 // fast path's +inf-key gating would not be equivalent).
 __device__ void walk_exact(const int S[3], const int E[3], const float g[3], const float s[3],
-                           const Dims& d, uint32_t* __restrict__ miss) {
+                           const Dims& d, uint32_t* __restrict__ miss, int y0, int y1,
+                           uint32_t inc) {
   int V[3] = {S[0], S[1], S[2]}, st[3], rem[3];
   float inv[3];
   for (int a = 0; a < 3; ++a) {
@@ -52,7 +53,7 @@ __device__ void walk_exact(const int S[3], const int E[3], const float g[3], con
   const int n[3] = {d.nx, d.ny, d.nz};
   while ((unsigned)V[0] < (unsigned)n[0] && (unsigned)V[1] < (unsigned)n[1] &&
          (unsigned)V[2] < (unsigned)n[2] && rem[0] + rem[1] + rem[2] > 0) {
-    atomicAdd(miss + (V[2] + d.nz * (V[0] + d.nx * V[1])), 1u);
+    if (V[1] >= y0 && V[1] < y1) atomicAdd(miss + (V[2] + d.nz * (V[0] + d.nx * V[1])), inc);
     int best = -1;
     float bk = 0.f;
     for (int a = 0; a < 3; ++a) {
@@ -139,6 +140,7 @@ __device__ void scan_tiles_if_last(const TileCounts& tc, const Dims& d) {
     tc.offset[i] = run;
     run += __ldcg(tc.tile + i);
   }
+  if (threadIdx.x == 0) *tc.done = 0u;  // every block has counted: ready for the next frame
 }
 
 // Miss increments of one warp step, merged over runs of adjacent lanes that
@@ -167,7 +169,9 @@ __device__ __forceinline__ void red_run(uint32_t* addr, bool head, uint32_t cnt)
       "r"(cnt), "r"((uint32_t)head));
 }
 
-// resident schedule: see above
+// resident schedule: see above.  kNeg: the run adds -count (the integrate
+// path counts misses down from -1 directly in the LUT: -1 - N_m, O6)
+template <bool kNeg>
 __device__ __forceinline__ void aggregate_red_resident(uint32_t* __restrict__ miss, uint32_t L,
                                                        bool active, bool lane0,
                                                        unsigned after_lanes, int lane) {
@@ -176,36 +180,36 @@ __device__ __forceinline__ void aggregate_red_resident(uint32_t* __restrict__ mi
   const bool brk = prev != key;
   const unsigned heads = __ballot_sync(0xffffffffu, brk);
   const bool head = active && (brk || lane0);
-#ifdef GVOM_RAY_CLZ
-  // run length = clz(brev(heads) & brev(after_lanes)) - lane (clz(0) = 32;
-  // brev(after_lanes) is loop-invariant and hoisted)
-  asm volatile(
-      "{ .reg .pred p; .reg .b32 t;\n\t"
-      "brev.b32 t, %1;\n\t"
-      "and.b32 t, t, %2;\n\t"
-      "clz.b32 t, t;\n\t"
-      "sub.u32 t, t, %3;\n\t"
-      "setp.ne.u32 p, %4, 0;\n\t"
-      "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
-      "r"(heads), "r"(__brev(after_lanes)), "r"(lane), "r"((uint32_t)head));
-  return;
-#endif
   // run length = distance to the next run start above this lane (32 if none):
   // ctz(x) = popc(~x & (x - 1)), which is 32 for x = 0 without a special case
-  asm volatile(
-      "{ .reg .pred p; .reg .b32 t, u;\n\t"
-      "and.b32 t, %1, %2;\n\t"
-      "add.u32 u, t, -1;\n\t"
-      "not.b32 t, t;\n\t"
-      "and.b32 t, t, u;\n\t"
-      "popc.b32 t, t;\n\t"
-      "sub.u32 t, t, %3;\n\t"
-      "setp.ne.u32 p, %4, 0;\n\t"
-      "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
-      "r"(heads), "r"(after_lanes), "r"(lane), "r"((uint32_t)head));
+  if (kNeg)
+    asm volatile(
+        "{ .reg .pred p; .reg .b32 t, u;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "add.u32 u, t, -1;\n\t"
+        "not.b32 t, t;\n\t"
+        "and.b32 t, t, u;\n\t"
+        "popc.b32 t, t;\n\t"
+        "sub.u32 t, %3, t;\n\t"
+        "setp.ne.u32 p, %4, 0;\n\t"
+        "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
+        "r"(heads), "r"(after_lanes), "r"(lane), "r"((uint32_t)head));
+  else
+    asm volatile(
+        "{ .reg .pred p; .reg .b32 t, u;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "add.u32 u, t, -1;\n\t"
+        "not.b32 t, t;\n\t"
+        "and.b32 t, t, u;\n\t"
+        "popc.b32 t, t;\n\t"
+        "sub.u32 t, t, %3;\n\t"
+        "setp.ne.u32 p, %4, 0;\n\t"
+        "@p red.relaxed.gpu.global.add.u32 [%0], t; }" ::"l"(miss_at<false>(miss, L)),
+        "r"(heads), "r"(after_lanes), "r"(lane), "r"((uint32_t)head));
 }
 
 // streaming schedule: `act` = the warp's active lanes
+template <bool kNeg>
 __device__ __forceinline__ void aggregate_red_stream(uint32_t* __restrict__ miss, uint32_t L,
                                                      bool active, unsigned act,
                                                      unsigned after_lanes, int lane) {
@@ -213,8 +217,8 @@ __device__ __forceinline__ void aggregate_red_stream(uint32_t* __restrict__ miss
   const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
   const bool head = active && (lane == 0 || prev != key);
   const unsigned heads = __ballot_sync(0xffffffffu, head);
-  const uint32_t cnt = (uint32_t)(__clz(__brev((heads | ~act) & after_lanes)) - lane);
-  red_run(miss_at<true>(miss, L), head, cnt);
+  const int run = __clz(__brev((heads | ~act) & after_lanes)) - lane;
+  red_run(miss_at<true>(miss, L), head, kNeg ? (uint32_t)(-run) : (uint32_t)run);
 }
 
 #ifndef GVOM_RAY_STREAM_BYTES
@@ -251,14 +255,14 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
 #endif
 constexpr int kRayUnroll = GVOM_RAY_UNROLL;
 // The step loop of a warp: one aggregated red per step, then one DDA step.
-template <bool kStream, class Step>
+template <bool kStream, bool kNeg, class Step>
 __device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uint32_t& L, int left,
                                           int lane, unsigned after_lanes, Step&& step) {
   if (kStream) {
     unsigned act = __ballot_sync(0xffffffffu, left > 0);
     while (act) {
       const bool active = left > 0;
-      aggregate_red_stream(miss, L, active, act, after_lanes, lane);
+      aggregate_red_stream<kNeg>(miss, L, active, act, after_lanes, lane);
       step();
       --left;
       act = __ballot_sync(0xffffffffu, left > 0);
@@ -270,17 +274,58 @@ __device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uin
 #pragma unroll (kRayUnroll)
     for (int it = 0; it < Tw; ++it) {
       const bool active = it < left;
-      aggregate_red_resident(miss, L, active, lane0, after_lanes, lane);
+      aggregate_red_resident<kNeg>(miss, L, active, lane0, after_lanes, lane);
       step();
     }
   }
 }
 
+// The step loop of a warp whose lanes walk steps [start_i, end_i) of their
+// rays (the ray-segment slab partition): iterations run over absolute step
+// indices, so lanes that reach a voxel at the same step still merge; a lane
+// holds its state until its start.
+template <bool kStream, bool kNeg, class Step>
+__device__ __forceinline__ void walk_loop_range(uint32_t* __restrict__ miss, const uint32_t& L,
+                                                int start, int end, int lane,
+                                                unsigned after_lanes, Step&& step) {
+  const bool has = start < end;
+  const int w0 = __reduce_min_sync(0xffffffffu, has ? start : 0x7fffffff);
+  const int w1 = __reduce_max_sync(0xffffffffu, has ? end : 0);
+  const bool lane0 = lane == 0;
+  for (int it = w0; it < w1; ++it) {
+    const bool active = it >= start && it < end;
+    if (kStream)
+      aggregate_red_stream<kNeg>(miss, L, active, __ballot_sync(0xffffffffu, active),
+                                 after_lanes, lane);
+    else
+      aggregate_red_resident<kNeg>(miss, L, active, lane0, after_lanes, lane);
+    if (it >= start) step();
+  }
+}
+
+// Steps taken once the walk has taken its c-th crossing of the y axis (axis 1):
+// that crossing, the c - 1 before it, and the x / z crossings that precede it in
+// the walk's (key, axis) order (x first on equal keys, z after) -- the index of
+// the first voxel of the walk beyond that y plane.  cnt[] = the crossings per axis.
+__device__ __forceinline__ int steps_through_y(const float eb[3], const float fb[3],
+                                               const float s[3], const float inv[3],
+                                               const int jm[3], int c, int cnt[3]) {
+  const float K = axis_key(eb[1], fb[1], s[1], inv[1], c);
+  cnt[0] = jm[0] > 0 ? count_before(eb[0], fb[0], s[0], inv[0], jm[0], K, true) : 0;
+  cnt[1] = c;
+  cnt[2] = jm[2] > 0 ? count_before(eb[2], fb[2], s[2], inv[2], jm[2], K, false) : 0;
+  return cnt[0] + c + cnt[2];
+}
+
 // The rays of one warp (32 consecutive thread ids gtid of the batch).
-template <bool kStream>
+// kSlab: only the steps whose voxel lies in rows [sr.y0, sr.y1) are traced and
+// only returns in those rows are binned (y is monotone along a walk, so that
+// is one step range [jin, jout), found exactly with the stateless keys).
+template <bool kStream, bool kNeg, bool kSlab = false>
 __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
                                          uint32_t* __restrict__ miss, uint32_t* __restrict__ bits,
-                                         const TileCounts& tc, int64_t gtid) {
+                                         const TileCounts& tc, int64_t gtid,
+                                         const SlabRange sr = SlabRange{0, 0}) {
   const int64_t gt = gtid / rb.tile_threads;  // interleaved (tile, sensor)
   const int sidx = (int)(gt % rb.S);
   const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
@@ -296,13 +341,15 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
   float e0 = 0.f, e1 = 0.f, e2 = 0.f, f0 = 0.f, f1 = 0.f, f2 = 0.f;
   float i0 = kInf, i1 = kInf, i2 = kInf, k0 = kInf, k1 = kInf, k2 = kInf;
   int dL0 = 0, dL1 = 0, dL2 = 0, left = 0;
+  int jm0 = 0, jm1 = 0, jm2 = 0;  // crossings each axis can take (kSlab)
+  int jin = 0;                    // kSlab: first step in the slab (left = its end)
   uint32_t L = 0;
   uint32_t newtile = 0xffffffffu;  // tile of a voxel this lane newly occupied
 
   if (p < n) {
-    const float4 q = __ldg(pts + p);
+    const float4 qp = __ldg(pts + p);
     float g[3];
-    if (transform_point(sp, q, g[0], g[1], g[2])) {
+    if (transform_point(sp, qp, g[0], g[1], g[2])) {
       const int n3[3] = {d.nx, d.ny, d.nz};
       const int strideY = d.nz * d.nx;
       const int str[3] = {d.nz, strideY, 1};
@@ -327,7 +374,7 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
       // endpoint occupancy (O4/O6: occupied iff hits >= 1); bits == nullptr in
       // the multi-GPU partial pass (occupancy is built on the slab owner)
       if (bits && (unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
-          (unsigned)E[2] < (unsigned)d.nz) {
+          (unsigned)E[2] < (unsigned)d.nz && (!kSlab || (E[1] >= sr.y0 && E[1] < sr.y1))) {
         const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
         const uint32_t bit = 1u << (LE & 31);
         newtile = (atomicOr(bits + (LE >> 5), bit) & bit) ? 0xffffffffu : (LE >> kTileShift);
@@ -386,7 +433,8 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
         }
         if (!ok) {
           const int S[3] = {sp.S[0], sp.S[1], sp.S[2]};
-          walk_exact(S, E, g, s, d, miss);
+          walk_exact(S, E, g, s, d, miss, kSlab ? sr.y0 : 0, kSlab ? sr.y1 : d.ny,
+                     kNeg ? 0xffffffffu : 1u);
           left = 0;
         } else {
           e0 = eb[0]; e1 = eb[1]; e2 = eb[2];
@@ -400,6 +448,46 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
           dL1 = st[1] * str[1] * unit;
           dL2 = st[2] * str[2] * unit;
           L = (uint32_t)(sp.S[2] + d.nz * sp.S[0] + strideY * sp.S[1]) * unit;
+          jm0 = rem[0] > 0 ? min(rem[0], room[0] + 1) : 0;
+          jm1 = rem[1] > 0 ? min(rem[1], room[1] + 1) : 0;
+          jm2 = rem[2] > 0 ? min(rem[2], room[2] + 1) : 0;
+          if (kSlab) {
+            // [jin, jout): the steps whose voxel row lies in [y0, y1)
+            const int Sy = sp.S[1];
+            const int jm[3] = {jm0, jm1, jm2};
+            int cnt[3] = {0, 0, 0};
+            int jout = left;
+            if (st[1] == 0) {
+              if (Sy < sr.y0 || Sy >= sr.y1) jout = 0;
+            } else {
+              // y crossings to enter / to leave the slab (0: inside from the start)
+              const int cin = st[1] > 0 ? (Sy < sr.y0 ? sr.y0 - Sy : 0)
+                                        : (Sy >= sr.y1 ? Sy - (sr.y1 - 1) : 0);
+              const bool before = st[1] > 0 ? Sy >= sr.y1 : Sy < sr.y0;  // already past
+              const int cout = st[1] > 0 ? sr.y1 - Sy : Sy - sr.y0 + 1;
+              if (before || cin > jm1) {
+                jout = 0;
+              } else {
+                if (cout <= jm1) {
+                  int c2[3];
+                  jout = min(jout, steps_through_y(eb, fb, s, inv, jm, cout, c2));
+                }
+                if (cin > 0) jin = steps_through_y(eb, fb, s, inv, jm, cin, cnt);
+              }
+            }
+            if (jin >= jout) {
+              jin = jout = 0;
+            } else if (jin > 0) {  // the walk's state at step jin
+              e0 = __fadd_rn(eb[0], fb[0] * (float)cnt[0]);
+              e1 = __fadd_rn(eb[1], fb[1] * (float)cnt[1]);
+              e2 = __fadd_rn(eb[2], fb[2] * (float)cnt[2]);
+              k0 = rem[0] > 0 ? __fmul_rn(__fsub_rn(e0, s0), i0) : kInf;
+              k1 = rem[1] > 0 ? __fmul_rn(__fsub_rn(e1, s1), i1) : kInf;
+              k2 = rem[2] > 0 ? __fmul_rn(__fsub_rn(e2, s2), i2) : kInf;
+              L += (uint32_t)(cnt[0] * dL0 + cnt[1] * dL1 + cnt[2] * dL2);
+            }
+            left = jout;
+          }
         }
       }
     }
@@ -412,7 +500,13 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
       atomicAdd(tc.tile + newtile, (uint32_t)__popc(peers));
   }
   const unsigned after_lanes = 0xfffffffeu << lane;  // lanes above this one
-  walk_loop<kStream>(miss, L, left, lane, after_lanes, [&] {
+  if (kSlab) {
+    walk_loop_range<kStream, kNeg>(miss, L, jin, left, lane, after_lanes, [&] {
+      dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
+    });
+    return;
+  }
+  walk_loop<kStream, kNeg>(miss, L, left, lane, after_lanes, [&] {
     dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
   });
 }
@@ -424,26 +518,28 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
 // The bound (kBS, 1) lets ptxas spend 68 registers (59 under a 256-thread
 // bound), which measured 8% faster on c5 and equal on c2; higher occupancy
 // (40 / 48 warps per SM at 48 / 40 registers) measured slower on every config.
-template <bool kStream, int kBS>
+// kNeg: misses count down from -1 in the slot's LUT (the integrate path, see
+// k_finalize_lut); else up from 0 in a plain miss grid (the multi-GPU partial
+// grids that are reduce-scattered).
+template <bool kStream, int kBS, bool kNeg>
 __global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayBatch rb,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
-#ifdef GVOM_RAY_SWZ
-  // block -> work bijection b -> b*P mod G (P coprime to G, near G/phi):
-  // spreads the ring pairs over the SMs of a one-wave frame
-  const uint32_t G = gridDim.x;
-  uint32_t P = (uint32_t)(0.6180339887 * G) | 1u;
-  for (;; P += 2) {
-    uint32_t a = P, b = G;
-    while (b) { const uint32_t t = a % b; a = b; b = t; }
-    if (a == 1 || P >= G) break;
-  }
-  const uint32_t bid = G > 2 ? (uint32_t)(((uint64_t)blockIdx.x * P) % G) : blockIdx.x;
-  ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)bid * blockDim.x + threadIdx.x);
-#else
-  ray_warp<kStream>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-#endif
+  ray_warp<kStream, kNeg>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (last_sensor && bits) scan_tiles_if_last(tc, d);
+}
+
+// Ray cast of the ray-segment slab partition: every ray of the frame, traced
+// only inside rows [sr.y0, sr.y1) (SURVEY 8(e) reworked).
+template <bool kStream, int kBS>
+__global__ void __launch_bounds__(kBS, 1) k_raycast_slab(const __grid_constant__ RayBatch rb,
+                                                      const Dims d, uint32_t* __restrict__ miss,
+                                                      uint32_t* __restrict__ bits,
+                                                      const TileCounts tc, bool last_sensor,
+                                                      const SlabRange sr) {
+  ray_warp<kStream, true, true>(rb, d, miss, bits, tc,
+                                (int64_t)blockIdx.x * blockDim.x + threadIdx.x, sr);
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
 
@@ -686,12 +782,13 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_tiles(
 // O4 per return: hits, min_dz, m1 = sum dz, m2 = sum dz^2 into the data row.
 // Returns of azimuth-adjacent lanes often share a voxel (ground near the
 // sensor): runs of equal voxels are reduced with a segmented shuffle
-// reduction and the run head issues the four atomics.
-__global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBatch rb,
-                                                  const Dims d, const int32_t* __restrict__ lut,
-                                                  gvom_voxel* __restrict__ data) {
+// reduction and the run head issues the four atomics.  Only returns in the
+// rows of `sr` are binned (the whole map, or a rank's slab).
+__device__ __forceinline__ void endpoint_warp(const RayBatch& rb, const Dims& d, int64_t gtid,
+                                              const int32_t* __restrict__ lut,
+                                              gvom_voxel* __restrict__ data,
+                                              const SlabRange sr) {
   // the batch's sensors interleaved by 32-column tile, as in k_raycast
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gt = gtid / rb.tile_threads;
   const int sidx = (int)(gt % rb.S);
   const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
@@ -707,7 +804,7 @@ __global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBat
     float g0, g1, g2;
     if (transform_point(sp, q, g0, g1, g2)) {
       const int e0 = (int)floorf(g0), e1 = (int)floorf(g1), e2 = (int)floorf(g2);
-      if ((unsigned)e0 < (unsigned)d.nx && (unsigned)e1 < (unsigned)d.ny &&
+      if ((unsigned)e0 < (unsigned)d.nx && e1 >= sr.y0 && e1 < sr.y1 &&
           (unsigned)e2 < (unsigned)d.nz) {
         valid = true;
         LE = (uint32_t)(e2 + d.nz * e0 + d.nz * d.nx * e1);
@@ -739,11 +836,111 @@ __global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBat
     }
   }
   if (head) {
-    gvom_voxel* row = data + __ldg(lut + LE);
+    const int32_t rank = __ldg(lut + LE);
+    gvom_voxel* row = data + rank;
     atomicAdd(&row->hits, cnt);
     atomicMin(&row->min_dz, mn);
     atomicAdd(reinterpret_cast<unsigned long long*>(&row->m1), (unsigned long long)s1);
     atomicAdd(reinterpret_cast<unsigned long long*>(&row->m2), (unsigned long long)s2);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBatch rb,
+                                                  const Dims d, const int32_t* __restrict__ lut,
+                                                  gvom_voxel* __restrict__ data,
+                                                  const SlabRange sr) {
+  endpoint_warp(rb, d, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, lut, data, sr);
+}
+
+// Integrate pass 0: the slot's LUT over tiles [t0, t1) set to -1 ("empty, no
+// misses", O6) and its occupancy bits cleared.  The ray cast then counts each
+// pass-through DOWN from -1 in place (kNeg), so an empty voxel's LUT entry is
+// already its final O6 code -1 - N_m (N_m <= points per frame <= 2^30: the
+// 2^30 saturation never applies, gvom_create checks the capacity), and the
+// finalize touches only occupied voxels.  Write-back stores for a LUT that
+// fits in L2 (the ray cast's reductions then hit L2), evict-first beyond.
+__global__ void __launch_bounds__(256) k_reset_slot(int32_t* __restrict__ lut, int64_t l0,
+                                                    int64_t l1, uint32_t* __restrict__ bits,
+                                                    int64_t w0, int64_t w1, bool keep) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // l0, w0 are tile starts: 16-byte aligned; tails (l1, w1 not multiples of 4) scalar
+  const int64_t n4 = (l1 - l0) >> 2, m4 = (w1 - w0) >> 2;
+  const int4 ones = make_int4(-1, -1, -1, -1);
+  const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+  int4* l4 = reinterpret_cast<int4*>(lut + l0);
+  uint4* b4 = reinterpret_cast<uint4*>(bits + w0);
+  for (int64_t i = i0; i < n4 + m4; i += stride) {
+    if (i < n4) {
+      if (keep)
+        l4[i] = ones;
+      else
+        __stcs(l4 + i, ones);
+    } else {
+      __stcs(b4 + (i - n4), zero);
+    }
+  }
+  if (i0 < 4) {
+    if (l0 + 4 * n4 + i0 < l1) lut[l0 + 4 * n4 + i0] = -1;
+    if (w0 + 4 * m4 + i0 < w1) bits[w0 + 4 * m4 + i0] = 0u;
+  }
+}
+
+// Integrate pass 1 (O6) over tiles [t0, t0 + gridDim.x): block b owns tile b
+// (256 bitmask words = 8192 voxels); its rank offset is the exclusive prefix
+// of the tile counts the ray cast kept and scanned, so no block waits on
+// another.  Per-word prefix (block scan) -> wprefix; each thread lists its
+// word's occupied voxels in shared memory at their rank within the tile, then
+// the block walks that list -- one occupied voxel per thread, loads
+// independent: the LUT entry holds -1 - misses (counted down by the ray
+// cast), it becomes the voxel's rank and its data row {0, misses, 0xFFFFFFFF,
+// 0, 0, 0} is initialised for the endpoint pass.  Empty voxels' entries are
+// final already.
+__global__ void __launch_bounds__(kTileWords) k_finalize_lut(
+    int32_t* __restrict__ lut, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
+    gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t0) {
+  __shared__ uint32_t wsum[kTileWords / 32];
+  __shared__ uint16_t slist[1 << kTileShift];  // occupied voxels of the tile, rank order
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t b = t0 + blockIdx.x;
+  const uint32_t off = __ldg(tc.offset + b);  // rank offset of this tile
+  const int64_t w = b * kTileWords + t;
+  const uint32_t bw = w < d.W ? __ldg(bits + w) : 0u;
+  const uint32_t c = __popc(bw);
+  const uint32_t inc = warp_incl_scan(c, lane);
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = lane < kTileWords / 32 ? wsum[lane] : 0u;
+    const uint32_t i = warp_incl_scan(v, lane);
+    if (lane < kTileWords / 32) wsum[lane] = i - v;
+  }
+  __syncthreads();
+  const uint32_t rel = wsum[wid] + inc - c;  // rank of the word's first voxel in the tile
+  const uint32_t pre = off + rel;
+  if (w < d.W) wprefix[w] = pre;
+  if (t == 0) tc.tile[b] = 0u;  // consumed by the ray cast's scan: zero for the next frame
+  uint32_t m = bw, j = rel;
+  while (m) {
+    slist[j++] = (uint16_t)(t * 32 + __ffs(m) - 1);
+    m &= m - 1u;
+  }
+  __shared__ uint32_t stotal;
+  if (t == kTileWords - 1) {
+    stotal = rel + c;
+    if (blockIdx.x == gridDim.x - 1) *tc.total = pre + c;  // k of the frame
+  }
+  __syncthreads();
+  const uint32_t n = stotal;
+  const int64_t vbase = b << kTileShift;
+  for (uint32_t i = t; i < n; i += kTileWords) {
+    const int64_t L = vbase + slist[i];
+    const uint32_t rank = off + i;
+    const uint32_t misses = (uint32_t)(-1 - lut[L]);
+    lut[L] = (int32_t)rank;
+    uint4* row = reinterpret_cast<uint4*>(data + rank);
+    row[0] = make_uint4(0u, misses, 0xffffffffu, 0u);
+    row[1] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -761,9 +958,25 @@ inline int64_t point_threads(int64_t n, int32_t rings) {
 #endif
 constexpr int kRayNarrowBS = GVOM_RAY_NARROW_BS;  // block size of one-wave frames (A/B switch)
 
+template <bool kNeg>
+static void launch_raycast_t(bool stream, bool wide, unsigned blocks, const RayBatch& rb,
+                             const Dims& d, uint32_t* miss, uint32_t* bits, const TileCounts& tc,
+                             bool last, cudaStream_t st) {
+  if (!stream && !wide)
+    k_raycast<false, kRayNarrowBS, kNeg><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss, bits, tc,
+                                                                          last);
+  else if (!stream)
+    k_raycast<false, 128, kNeg><<<blocks, 128, 0, st>>>(rb, d, miss, bits, tc, last);
+  else if (!wide)
+    k_raycast<true, kRayNarrowBS, kNeg><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss, bits, tc,
+                                                                         last);
+  else
+    k_raycast<true, 128, kNeg><<<blocks, 128, 0, st>>>(rb, d, miss, bits, tc, last);
+}
+
 cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_grid,
                            uint32_t* bits, const TileCounts& tc, bool last_launch,
-                           cudaStream_t st) {
+                           cudaStream_t st, const SlabRange* slab, bool lut_direct) {
   int64_t tiles = 0;  // per sensor, the batch's maximum
   for (int s = 0; s < rb.S; ++s) {
     const int64_t t = (point_threads(rb.n[s], rb.rings) + rb.tile_threads - 1) / rb.tile_threads;
@@ -781,16 +994,25 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   const int64_t miss_bytes = (int64_t)d.nx * d.ny * d.nz * 4;
   const int64_t resident_max = kRayStreamBytes > 0 ? kRayStreamBytes : d.l2_bytes / 2;
   const bool stream = !(miss_bytes <= resident_max && miss_bytes < (int64_t(1) << 32));
-  if (!stream && !wide)
-    k_raycast<false, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss_grid, bits, tc,
-                                                                    last_launch);
-  else if (!stream)
-    k_raycast<false, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
-  else if (!wide)
-    k_raycast<true, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(rb, d, miss_grid, bits, tc,
-                                                                   last_launch);
+  if (slab && (slab->y0 > 0 || slab->y1 < d.ny)) {  // ray-segment slab partition (LUT-direct)
+    if (!stream && !wide)
+      k_raycast_slab<false, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(
+          rb, d, miss_grid, bits, tc, last_launch, *slab);
+    else if (!stream)
+      k_raycast_slab<false, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch,
+                                                         *slab);
+    else if (!wide)
+      k_raycast_slab<true, kRayNarrowBS><<<blocks, kRayNarrowBS, 0, st>>>(
+          rb, d, miss_grid, bits, tc, last_launch, *slab);
+    else
+      k_raycast_slab<true, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch,
+                                                        *slab);
+    return cudaGetLastError();
+  }
+  if (lut_direct)
+    launch_raycast_t<true>(stream, wide, blocks, rb, d, miss_grid, bits, tc, last_launch, st);
   else
-    k_raycast<true, 128><<<blocks, 128, 0, st>>>(rb, d, miss_grid, bits, tc, last_launch);
+    launch_raycast_t<false>(stream, wide, blocks, rb, d, miss_grid, bits, tc, last_launch, st);
   return cudaGetLastError();
 }
 
@@ -835,8 +1057,40 @@ cudaError_t launch_finalize_tiles(int32_t* lut_inplace, const uint32_t* bits, ui
   return cudaGetLastError();
 }
 
+cudaError_t launch_reset_slot(int32_t* lut, uint32_t* bits, const Dims& d, int64_t t0,
+                              int64_t t1, cudaStream_t st) {
+  const int64_t l0 = t0 << kTileShift, l1 = min(d.V, t1 << kTileShift);
+  const int64_t w0 = t0 * kTileWords, w1 = min(d.W, t1 * kTileWords);
+  if (l1 <= l0) return cudaSuccess;
+  const int64_t n = (l1 - l0) / 4 + (w1 - w0) / 4;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)d.sms * 8) blocks = (int64_t)d.sms * 8;
+  if (blocks < 1) blocks = 1;
+  static int use_memset = -1;  // GVOM_RESET_MEMSET=1: two driver memsets (A/B)
+  if (use_memset < 0) {
+    const char* e = getenv("GVOM_RESET_MEMSET");
+    use_memset = e && atoi(e) ? 1 : 0;
+  }
+  if (use_memset) {
+    cudaError_t e = cudaMemsetAsync(lut + l0, 0xff, 4 * (size_t)(l1 - l0), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bits + w0, 0, 4 * (size_t)(w1 - w0), st);
+    return e;
+  }
+  const bool keep = 4 * (l1 - l0) <= 3 * d.l2_bytes / 4;  // the REDs then hit L2
+  k_reset_slot<<<(unsigned)blocks, 256, 0, st>>>(lut, l0, l1, bits, w0, w1, keep);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_lut(int32_t* lut, const uint32_t* bits, uint32_t* wprefix,
+                                gvom_voxel* data, const TileCounts& tc, const Dims& d, int64_t t0,
+                                int64_t t1, cudaStream_t st) {
+  if (t1 <= t0) return cudaSuccess;
+  k_finalize_lut<<<(unsigned)(t1 - t0), kTileWords, 0, st>>>(lut, bits, wprefix, data, tc, d, t0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lut,
-                            gvom_voxel* data, cudaStream_t st) {
+                            gvom_voxel* data, cudaStream_t st, const SlabRange& slab) {
   int64_t tiles = 0;  // per sensor, the batch's maximum
   for (int s = 0; s < rb.S; ++s) {
     const int64_t t = (point_threads(rb.n[s], rb.rings) + rb.tile_threads - 1) / rb.tile_threads;
@@ -844,7 +1098,7 @@ cudaError_t launch_endpoint(const RayBatch& rb, const Dims& d, const int32_t* lu
   }
   const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
-  k_endpoint<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(rb, d, lut, data);
+  k_endpoint<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(rb, d, lut, data, slab);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 //   negative: 4-cone Chebyshev-ring search over undefined cells
 //   merge_* : full combined voxel map (LUT + data) for export
 #include <math.h>
+#include <stdlib.h>
 
 #include "gvom_internal.cuh"
 
@@ -373,6 +374,116 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   out.rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
 }
 
+// The same plane fit with the defined cells compacted: a 32 x 16 tile (+ the
+// r-cell halo) per 256-thread block; undefined cells are written NaN by the
+// thread that classifies them, the defined ones go into a block list (warp
+// ballots + a block prefix) that all threads then share, so every lane of a
+// warp fits a plane (the per-cell kernel ran ~12 of 32 lanes: undefined
+// centres, the double atan's branches).  The finish is atanf of the exact
+// normal-equation gradient (within ~2 ulp f32 of the double atan, well inside
+// the contract's 1e-4 + 1e-5 |ref|); the nodata decisions are unchanged
+// integer tests.
+constexpr int kSlope2TX = 32, kSlope2TY = 16;
+__global__ void __launch_bounds__(256) k_slope_c(const Dims d, const LayerParams lp,
+                                                 const LayerPtrs out) {
+  constexpr int SW_ = kSlope2TX + 2 * kSlopeHalo, SH_ = kSlope2TY + 2 * kSlopeHalo;
+  __shared__ int32_t tile[SH_][SW_ + 1];
+  __shared__ uint16_t list[kSlope2TX * kSlope2TY];
+  __shared__ uint32_t cnt[16];
+  const int r = (lp.slope_window - 1) / 2;
+  const int x0 = blockIdx.x * kSlope2TX, y0 = lp.row0 + blockIdx.y * kSlope2TY;
+  const int32_t* __restrict__ qs = out.qs;
+  for (int i = threadIdx.x; i < SW_ * SH_; i += 256) {
+    const int ty = i / SW_, tx = i % SW_;
+    const int gx = x0 + tx - kSlopeHalo, gy = y0 + ty - kSlopeHalo;
+    int32_t q = kQsUndef;
+    if ((unsigned)gx < (unsigned)d.nx && (unsigned)gy < (unsigned)d.ny) {
+      const int64_t cc = gx + (int64_t)d.nx * gy;
+      q = __ldg(qs + cc);
+      if (lp.skip_obstacles && (__ldg(out.hard + cc) | __ldg(out.soft + cc))) q = kQsUndef;
+    }
+    tile[ty][tx] = q;
+  }
+  __syncthreads();
+  const float qnan = __int_as_float(0x7fc00000);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned bal[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // warp w classifies rows 2w and 2w + 1
+    const int ty = 2 * warp + h, x = x0 + lane, y = y0 + ty;
+    const bool inmap = x < d.nx && y < lp.row1;
+    const bool def = inmap && tile[ty + kSlopeHalo][lane + kSlopeHalo] != kQsUndef;
+    if (inmap && !def) {
+      const int64_t c = x + (int64_t)d.nx * y;
+      out.slope[c] = qnan;
+      out.rough[c] = qnan;
+    }
+    bal[h] = __ballot_sync(0xffffffffu, def);
+    if (lane == 0) cnt[2 * warp + h] = __popc(bal[h]);
+  }
+  __syncthreads();
+  uint32_t total = 0, base[2] = {0u, 0u};
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t v = cnt[j];
+    if (j == 2 * warp) base[0] = total;
+    if (j == 2 * warp + 1) base[1] = total;
+    total += v;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if ((bal[h] >> lane) & 1u)
+      list[base[h] + __popc(bal[h] & ((1u << lane) - 1u))] =
+          (uint16_t)((2 * warp + h) * kSlope2TX + lane);
+  __syncthreads();
+  for (uint32_t it = threadIdx.x; it < total; it += 256) {
+    const int li = list[it];
+    const int tx = li % kSlope2TX, ty = li / kSlope2TX;
+    const int64_t c = (x0 + tx) + (int64_t)d.nx * (y0 + ty);
+    const int cx = tx + kSlopeHalo, cy = ty + kSlopeHalo;
+    const int32_t qc = tile[cy][cx];
+    int32_t n = 0, Su = 0, Sv = 0, Suu = 0, Svv = 0, Suv = 0;
+    int64_t Sz = 0, Suz = 0, Svz = 0;
+    for (int v = -r; v <= r; ++v)
+      for (int u = -r; u <= r; ++u) {
+        const int32_t q = tile[cy + v][cx + u];
+        if (q == kQsUndef) continue;
+        const int64_t z = (int64_t)q - qc;
+        n += 1;
+        Su += u;
+        Sv += v;
+        Suu += u * u;
+        Svv += v * v;
+        Suv += u * v;
+        Sz += z;
+        Suz += u * z;
+        Svz += v * z;
+      }
+    const int64_t det = det3(Suu, Suv, Su, Suv, Svv, Sv, Su, Sv, n);
+    if (n < lp.min_plane_points || det == 0) {
+      out.slope[c] = qnan;
+      out.rough[c] = qnan;
+      continue;
+    }
+    const int64_t Da = det3(Suz, Suv, Su, Svz, Svv, Sv, Sz, Sv, n);
+    const int64_t Db = det3(Suu, Suz, Su, Suv, Svz, Sv, Su, Sz, n);
+    const int64_t Dc = det3(Suu, Suv, Suz, Suv, Svv, Svz, Su, Sv, Sz);
+    const double a = (double)Da / ((double)det * 65536.0);
+    const double b = (double)Db / ((double)det * 65536.0);
+    out.slope[c] = atanf((float)sqrt(a * a + b * b));
+    double acc = 0.0;
+    for (int v = -r; v <= r; ++v)
+      for (int u = -r; u <= r; ++u) {
+        const int32_t q = tile[cy + v][cx + u];
+        if (q == kQsUndef) continue;
+        const int64_t z = (int64_t)q - qc;
+        const double e = (double)(det * z - Da * u - Db * v - Dc);
+        acc += e * e;
+      }
+    const double sc = lp.res / 65536.0;
+    out.rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
+  }
+}
+
 // O10 cone search as a sweep.  For cone +x, let D(x,y) be the first ring k
 // (1..K) whose column segment {(x+k, y+t): |t| <= k} holds a defined cell,
 // and Mn / Mx the min / max q_s over the defined cells of that ring.  Ring k
@@ -442,12 +553,19 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   const bool alongx = cone < 2;              // sweep over x (lines = columns)
   const int dir = (cone & 1) ? -1 : 1;       // ring lines lie at p + dir*k
   const int A = alongx ? d.nx : d.ny;        // lines
-  const int B = alongx ? d.ny : d.nx;        // cross positions per line
   const int K = lp.neg_cells;
+  const int LB = alongx ? d.ny : d.nx;       // keys per source line
+  int c0 = 0, c1 = LB;                       // cross positions held (k_negative_tb)
+  if (alongx) {
+    c0 = max(0, (lp.row0 - K - 1) & ~3);
+    c1 = min(LB, (lp.row1 + K + 1 + 3) & ~3);
+  }
+  const int B = c1 - c0;                     // cross positions per line
   const int NB = B + 2 * K + 2;              // apex cross positions -K-1 .. B+K
   const int GL = neg_guard_left(K);
   const int LS = neg_line_stride(B, K);      // one key line (A or B keys)
   const int nthr = blockDim.x - 32;          // consumer threads
+  const int e0 = alongx ? 0 : lp.row0, e1 = alongx ? d.nx : lp.row1;  // lines emitted
   const uint32_t ONE = 1u << lp.neg_qb;
   const uint32_t NF = (uint32_t)(K + 1) << lp.neg_qb;  // not found
   const uint32_t QM = ONE - 1u;
@@ -456,11 +574,11 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
   uint32_t* An = Ap + NB;
   uint32_t* Bp = An + NB;
   uint32_t* Bn = Bp + NB;
-  const uint32_t* __restrict__ srcA = alongx ? out.negAT : out.negA;  // line-contiguous
-  const uint32_t* __restrict__ srcB = alongx ? out.negBT : out.negB;
-  const int p0 = blockIdx.x * T;             // tile lines [p0, p0+T)
-  if (p0 >= A) return;                       // grid sized for max(nx, ny)
-  const int p1 = min(A, p0 + T);
+  const uint32_t* __restrict__ srcA = (alongx ? out.negAT : out.negA) + c0;  // line-contiguous
+  const uint32_t* __restrict__ srcB = (alongx ? out.negBT : out.negB) + c0;
+  const int p0 = e0 + blockIdx.x * T;        // tile lines [p0, p0+T)
+  if (p0 >= e1) return;                      // grid sized for the longest cone
+  const int p1 = min(e1, p0 + T);
   int pstart, nsteps;                        // apex lines, in sweep order
   if (dir > 0) {
     pstart = min(A - 1, p1 - 1 + K);
@@ -469,7 +587,7 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
     pstart = max(0, p0 - K);
     nsteps = p1 - pstart;
   }
-  const bool tma = (B & 3) == 0;             // rows are whole 16-byte chunks
+  const bool tma = (B & 3) == 0 && (LB & 3) == 0;  // rows are whole 16-byte chunks
   const uint32_t line_bytes = (uint32_t)B * 4u;
   auto line_of = [&](int st) { return pstart - dir * st + dir; };  // ring-1 line of step st
   for (int i = threadIdx.x; i < NB; i += blockDim.x) {
@@ -503,8 +621,8 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
                        "r"(2u * line_bytes)
                        : "memory");
-          tma_copy(dst, srcA + (int64_t)pl * B, line_bytes, &full[j]);
-          tma_copy(dst + LS, srcB + (int64_t)pl * B, line_bytes, &full[j]);
+          tma_copy(dst, srcA + (int64_t)pl * LB, line_bytes, &full[j]);
+          tma_copy(dst + LS, srcB + (int64_t)pl * LB, line_bytes, &full[j]);
         } else {
           mbar_arrive(&full[j]);
         }
@@ -529,8 +647,8 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
     mbar_wait(&full[j], ph);
     if (inmap && !tma) {  // rows not 16-byte multiples: plain loads
       for (int b = threadIdx.x; b < B; b += nthr) {
-        la[GL + b] = __ldg(srcA + (int64_t)pl * B + b);
-        lb[GL + b] = __ldg(srcB + (int64_t)pl * B + b);
+        la[GL + b] = __ldg(srcA + (int64_t)pl * LB + b);
+        lb[GL + b] = __ldg(srcB + (int64_t)pl * LB + b);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
     }
@@ -548,9 +666,10 @@ __global__ void __launch_bounds__(1024) k_negative(const Dims d, const LayerPara
       kb = min(kb, NF);
       An[i] = ka;
       Bn[i] = kb;
-      const int b = i - K - 1;
-      if (emit && ka < NF && (unsigned)b < (unsigned)B) {
-        const int64_t cell = alongx ? (int64_t)b * d.nx + p : (int64_t)p * d.nx + b;
+      const int b = i - K - 1, bg = b + c0;
+      if (emit && ka < NF && (unsigned)b < (unsigned)B &&
+          (!alongx || (bg >= lp.row0 && bg < lp.row1))) {
+        const int64_t cell = alongx ? (int64_t)bg * d.nx + p : (int64_t)p * d.nx + bg;
         atomicMin(out.nmin + cell, (int32_t)(ka & QM));
         atomicMax(out.nmax + cell, (int32_t)(QM - (kb & QM)));
       }
@@ -703,23 +822,33 @@ __global__ void __launch_bounds__(1024) k_negative_tb(const Dims d, const LayerP
   const bool alongx = cone < 2;              // sweep over x (lines = columns)
   const int dir = (cone & 1) ? -1 : 1;       // ring lines lie at p + dir*k
   const int A = alongx ? d.nx : d.ny;        // lines
-  const int B = alongx ? d.ny : d.nx;        // cross positions per line
   const int K = lp.neg_cells;
+  // cross positions held: a line's keys [c0, c1) (rows [row0, row1) of a slab
+  // plus a K + 1 halo for the x sweeps; the cells beyond count as outside the
+  // map, which cannot reach an emitted cell: its cone spans +-K cross cells)
+  const int LB = alongx ? d.ny : d.nx;       // keys per source line
+  int c0 = 0, c1 = LB;
+  if (alongx) {
+    c0 = max(0, (lp.row0 - K - 1) & ~3);
+    c1 = min(LB, (lp.row1 + K + 1 + 3) & ~3);
+  }
+  const int B = c1 - c0;                     // cross positions per line
   const int NB = B + 2 * K + 2;              // apex cross positions -K-1 .. B+K
   const int GL = neg_guard_left(K);
   const int LS = neg_line_stride(B, K);
   const int nthr = W * 32;                   // consumer threads
+  const int e0 = alongx ? 0 : lp.row0, e1 = alongx ? d.nx : lp.row1;  // lines emitted
   const uint32_t ONE = 1u << lp.neg_qb;
   const uint32_t NF = (uint32_t)(K + 1) << lp.neg_qb;  // not found
   const uint32_t QM = ONE - 1u;
   uint32_t* ring = sm;                       // [R][2][LS]
   uint32_t* SA = ring + (size_t)R * 2 * LS;  // [2][NB] owned A keys (double buffer)
   uint32_t* SB = SA + 2 * NB;                // [2][NB] owned B keys
-  const uint32_t* __restrict__ srcA = alongx ? out.negAT : out.negA;
-  const uint32_t* __restrict__ srcB = alongx ? out.negBT : out.negB;
-  const int p0 = blockIdx.x * T;
-  if (p0 >= A) return;
-  const int p1 = min(A, p0 + T);
+  const uint32_t* __restrict__ srcA = (alongx ? out.negAT : out.negA) + c0;
+  const uint32_t* __restrict__ srcB = (alongx ? out.negBT : out.negB) + c0;
+  const int p0 = e0 + blockIdx.x * T;
+  if (p0 >= e1) return;
+  const int p1 = min(e1, p0 + T);
   int pstart, nsteps;
   if (dir > 0) {
     pstart = min(A - 1, p1 - 1 + K);
@@ -759,8 +888,8 @@ __global__ void __launch_bounds__(1024) k_negative_tb(const Dims d, const LayerP
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
                        "r"(2u * line_bytes)
                        : "memory");
-          tma_copy(dst, srcA + (int64_t)pl * B, line_bytes, &full[j]);
-          tma_copy(dst + LS, srcB + (int64_t)pl * B, line_bytes, &full[j]);
+          tma_copy(dst, srcA + (int64_t)pl * LB, line_bytes, &full[j]);
+          tma_copy(dst + LS, srcB + (int64_t)pl * LB, line_bytes, &full[j]);
         } else {
           mbar_arrive(&full[j]);
         }
@@ -817,9 +946,10 @@ __global__ void __launch_bounds__(1024) k_negative_tb(const Dims d, const LayerP
         kb = live[s] ? min(kb, NF) : NF;
         a[s] = ka;
         b[s] = kb;
-        const int bx = i - K - 1;
-        if (emit && owner && ka < NF && (unsigned)bx < (unsigned)B) {
-          const int64_t cell = alongx ? (int64_t)bx * d.nx + p : (int64_t)p * d.nx + bx;
+        const int bx = i - K - 1, bg = bx + c0;
+        if (emit && owner && ka < NF && (unsigned)bx < (unsigned)B &&
+            (!alongx || (bg >= lp.row0 && bg < lp.row1))) {
+          const int64_t cell = alongx ? (int64_t)bg * d.nx + p : (int64_t)p * d.nx + bg;
           atomicMin(out.nmin + cell, (int32_t)(ka & QM));
           atomicMax(out.nmax + cell, (int32_t)(QM - (kb & QM)));
         }
@@ -847,8 +977,8 @@ __global__ void __launch_bounds__(1024) k_negative_tb(const Dims d, const LayerP
 // max F - min F > T_neg (T_neg >= 0, so this implies |F| >= 2, reading B2)
 __global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerParams lp,
                                                     const LayerPtrs out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= (int64_t)d.nx * d.ny) return;
+  const int64_t c = (int64_t)lp.row0 * d.nx + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (int64_t)lp.row1 * d.nx) return;
   const int32_t mn = __ldg(out.nmin + c), mx = __ldg(out.nmax + c);
   out.neg[c] = (__ldg(out.qs + c) == kQsUndef && mx != INT32_MIN &&
                 (int64_t)mx - (int64_t)mn > lp.T_neg)
@@ -1013,8 +1143,19 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
 
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st) {
-  const dim3 grid((d.nx + kSlopeTX - 1) / kSlopeTX, (d.ny + kSlopeTY - 1) / kSlopeTY);
-  k_slope<<<grid, dim3(kSlopeTX, kSlopeTY), 0, st>>>(d, lp, out);
+  static int old_kernel = -1;  // GVOM_SLOPE_PERCELL=1: the per-cell kernel (A/B)
+  if (old_kernel < 0) {
+    const char* e = getenv("GVOM_SLOPE_PERCELL");
+    old_kernel = e && atoi(e) ? 1 : 0;
+  }
+  if (old_kernel) {
+    const dim3 grid((d.nx + kSlopeTX - 1) / kSlopeTX, (d.ny + kSlopeTY - 1) / kSlopeTY);
+    k_slope<<<grid, dim3(kSlopeTX, kSlopeTY), 0, st>>>(d, lp, out);
+  } else {
+    const int rows = lp.row1 - lp.row0;
+    const dim3 grid((d.nx + kSlope2TX - 1) / kSlope2TX, (rows + kSlope2TY - 1) / kSlope2TY);
+    k_slope_c<<<grid, 256, 0, st>>>(d, lp, out);
+  }
   return cudaGetLastError();
 }
 
@@ -1025,10 +1166,12 @@ inline bool neg_tb_enabled() { return GVOM_NEG_TB != 0; }  // A/B knob
 
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                             cudaStream_t st) {
-  const int A = d.nx > d.ny ? d.nx : d.ny, B = A;
+  const int A = d.nx > d.ny ? d.nx : d.ny, B = A;  // smem sized for the longest line
   const int K = lp.neg_cells;
-  // tiles: about one block per SM over the 4 cones, at least 8 lines each
-  int T = (4 * A + d.sms - 1) / d.sms;
+  // tiles: about one block per SM over the emitted lines of the 4 cones (rows
+  // [row0, row1) for the y sweeps, every column for the x sweeps), >= 8 lines
+  const int rows = lp.row1 - lp.row0;
+  int T = (2 * d.nx + 2 * rows + d.sms - 1) / d.sms;
   T = T < 8 ? 8 : ((T + 7) / 8) * 8;
 #ifdef GVOM_NEG_T
   T = GVOM_NEG_T;
@@ -1040,13 +1183,23 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   if (!neg_sweep_fits(B, K)) return cudaErrorInvalidConfiguration;
   int R = (int)((kNegSmemMax - state) / slot);
   R = R > kNegRing ? kNegRing : R;
+  {  // GVOM_NEG_RMAX: cap the ring depth (A/B: leaves shared memory for the
+     // plane-fit blocks that run concurrently on the main stream)
+    static int rmax = -1;
+    if (rmax < 0) {
+      const char* e = getenv("GVOM_NEG_RMAX");
+      rmax = e ? atoi(e) : 0;
+    }
+    if (rmax >= 2 && R > rmax) R = rmax;
+  }
   const size_t smem = state + (size_t)R * slot;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(
         k_negative, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  const dim3 grid((unsigned)((A + T - 1) / T), 4);
+  const int lines = d.nx > rows ? d.nx : rows;
+  const dim3 grid((unsigned)((lines + T - 1) / T), 4);
   // temporally blocked sweep when the rows of both sweep directions are whole
   // 16-byte chunks (TMA) and up to 4 segments per warp (31 warps) cover a
   // line: c2 18.3 -> 15.1 us, c4 29.4 -> 27.0 us, c5 (2 segments) 110 -> 97 us
@@ -1072,7 +1225,8 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   }
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_neg_decide<<<cells_blocks(d, 256), 256, 0, st>>>(d, lp, out);
+  const int64_t dc = (int64_t)(lp.row1 - lp.row0) * d.nx;
+  k_neg_decide<<<(unsigned)((dc + 255) / 256), 256, 0, st>>>(d, lp, out);
   return cudaGetLastError();
 }
 

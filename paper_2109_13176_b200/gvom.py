@@ -88,6 +88,7 @@ def load_library() -> C.CDLL:
         "gvom_synchronize": ([P], I32),
         "gvom_shift": ([P, P, P], I32),
         "gvom_integrate_scan": ([P, P, I32], I32),
+        "gvom_integrate_slab": ([P, P, I32, I32, I32], I32),
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
         "gvom_export_layers": ([P, P, P], I32),
@@ -132,7 +133,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
             "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers",
-            "gvom_obstacle_buffers", "gvom_debug_inject_fault")
+            "gvom_obstacle_buffers", "gvom_debug_inject_fault", "gvom_integrate_slab")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -338,7 +339,7 @@ class GvomMap:
         """(hard, soft): uint8 [ny, nx] views of the library's obstacle layers."""
         hp, sp_ = C.c_void_p(), C.c_void_p()
         _check(self.lib.gvom_obstacle_buffers(self.h, C.byref(hp), C.byref(sp_)),
-               "gvom_obstacle_buffers", "gvom_debug_inject_fault")
+               "gvom_obstacle_buffers")
         n = self.nx * self.ny
         views = []
         for ptr in (hp, sp_):
@@ -354,6 +355,14 @@ class GvomMap:
         rc = self.lib.gvom_integrate_scan(self.h, arr, n)
         _check(rc, "gvom_integrate_scan")
         self._retain(keep)  # input buffers must live until the stream passes
+
+    def integrate_slab(self, scans: Iterable[ScanLike], y0: int, y1: int):
+        """Ray-segment slab partition: every sensor of the frame, traced and
+        binned only inside map rows [y0, y1) (local data ranks)."""
+        arr, n, keep = self._scan_array(scans)
+        _check(self.lib.gvom_integrate_slab(self.h, arr, n, int(y0), int(y1)),
+               "gvom_integrate_slab")
+        self._retain(keep)
 
     def compute_maps(self):
         _check(self.lib.gvom_compute_maps(self.h), "gvom_compute_maps")

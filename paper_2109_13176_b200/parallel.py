@@ -1,5 +1,16 @@
 """Multi-GPU slab partition of one frame, collectives only.
 
+Two partitions of the same frame, both exact (identical to one GPU):
+
+* ray segments (SegmentMapper, the default of bench.py): every rank receives
+  every sensor's points (all_gather_scans: 16 bytes per point) and
+  gvom_integrate_slab traces only the part of each ray inside its own rows --
+  no dense count grid leaves a GPU, nothing is reduced; the surface rows are
+  all-gathered for the plane fits and the cone search.
+* reduce-scatter (SlabMapper, the north_star's design): every rank traces its
+  own sensors' rays whole into a dense partial miss grid, and the grids are
+  combined by slab as below.
+
 One process per GPU (torch.distributed, NCCL over NVLink; gloo on CPU for the
 tests).  Rank r of P owns the y-rows [y_r, y_{r+1}) of the map; in L order
 (z + nz*(x + nx*y)) that is one contiguous voxel range, so the exchange is:
@@ -159,4 +170,79 @@ class SlabMapper:
         if int(self.m.cfg.flags) & 2:  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES: windows read them
             for t in self.m.obstacles():
                 gather_rows(t, self.y0, self.y1, self.group)
+        self.m.compute_maps_slab(self.y0, self.y1, 1)
+
+
+# ---------------------------------------------------------------------------
+# ray-segment partition
+# ---------------------------------------------------------------------------
+def all_gather_scans(scans, group=None):
+    """Every rank's sensors -> every rank, in (rank, local order): a list of
+    (points [n, 4] f32, pose [3, 4], rings) on this rank's device.  Metadata
+    with all_gather_object, the points as one padded all_gather_into_tensor."""
+    import numpy as np
+    P = dist.get_world_size(group)
+    dev = scans[0][0].device if scans else (
+        torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() and
+        dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    meta = [(int(p.shape[0]), np.asarray(pose, np.float64).reshape(3, 4).tolist(), int(rings))
+            for (p, pose, rings) in scans]
+    metas = [None] * P
+    dist.all_gather_object(metas, meta, group=group)
+    tot = [sum(n for n, _, _ in m) for m in metas]
+    cap = max(max(tot), 1)
+    mine = torch.zeros((cap, 4), dtype=torch.float32, device=dev)
+    if scans:
+        flat = torch.cat([p.to(dev, torch.float32).reshape(-1, 4) for (p, _, _) in scans])
+        mine[:flat.shape[0]] = flat
+    allp = torch.empty((P * cap, 4), dtype=torch.float32, device=dev)
+    dist.all_gather_into_tensor(allp, mine, group=group)
+    out = []
+    for r in range(P):
+        off = r * cap
+        for n, pose, rings in metas[r]:
+            out.append((allp[off:off + n], np.asarray(pose, np.float64), rings))
+            off += n
+    return out
+
+
+def global_rank_base(k_local: torch.Tensor, group=None):
+    """Local data ranks -> global: (this slab's base, total k) from the slabs'
+    occupied counts (device scalar in, device scalars out: no host sync)."""
+    P = dist.get_world_size(group)
+    allk = torch.empty(P, dtype=k_local.dtype, device=k_local.device)
+    dist.all_gather_into_tensor(allk, k_local.reshape(1), group=group)
+    r = dist.get_rank(group)
+    return allk[:r].sum(), allk.sum()
+
+
+class SegmentMapper:
+    """Drives one rank's GvomMap through the ray-segment partition: all
+    sensors of the frame are gathered, the rank traces and bins only its rows
+    (gvom_integrate_slab), computes the columns of its rows, and the surface
+    rows are all-gathered for phase 1 (slope / roughness / cone search)."""
+
+    def __init__(self, m, group=None):
+        self.m = m
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.ys = slab_rows(m.ny, self.P)
+        self.y0, self.y1 = self.ys[self.rank], self.ys[self.rank + 1]
+
+    def integrate(self, scans_local, gathered: bool = False):
+        """scans_local: this rank's sensors (gathered=True: already all of them)."""
+        scans = scans_local if gathered else all_gather_scans(scans_local, self.group)
+        torch.cuda.current_stream(self.m.device).wait_stream(torch.cuda.current_stream())
+        self.m.integrate_slab(scans, self.y0, self.y1)
+
+    def compute_maps(self):
+        self.m.compute_maps_slab(self.y0, self.y1, 0)
+        cur = torch.cuda.current_stream(self.m.device)
+        cur.wait_stream(self.m.stream)
+        gather_rows(self.m.surface(), self.y0, self.y1, self.group)
+        if int(self.m.cfg.flags) & 2:  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES: windows read them
+            for t in self.m.obstacles():
+                gather_rows(t, self.y0, self.y1, self.group)
+        self.m.stream.wait_stream(cur)
         self.m.compute_maps_slab(self.y0, self.y1, 1)

@@ -56,6 +56,19 @@ def test_c3_motion_sequence(speed):
     run_sequence(w, check_every=4)
 
 
+@pytest.mark.parametrize("speed,use_step", [(4.5, False), (12.0, True)])
+def test_c3_baseline_shape_sequence(speed, use_step):
+    # BASELINE configs[2] at its own shape: OS1-128 x 2048 = 262,144 points per
+    # scan, 24 scans at 10 Hz and 4.5 / 12 m/s, K = 8: frame map,
+    # layers and the merged voxel map compared every 4th frame; the 12 m/s run
+    # goes through gvom_step, the graphed call bench.py times
+    w = synth.config3(speed=speed, n_frames=24)
+    assert w.points_per_frame == 262144
+    m, _ = run_sequence(w, check_every=4, use_step=use_step)
+    if use_step:
+        assert m.graph_stats()["graph_launches"] == 24
+
+
 def test_c4_three_lidars_full_size():
     run_sequence(synth.workload(3))
 

@@ -97,8 +97,8 @@ def _run(w, P, peers=False, **over):
         for k_ in ("height", "density", "hard", "soft"):
             a, b = lay[k_][sl], ref_layers[k_][sl]
             assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
-        for k_ in ("slope", "roughness", "neg"):
-            a, b = lay[k_], ref_layers[k_]
+        for k_ in ("slope", "roughness", "neg"):  # phase 1 is slab-local
+            a, b = lay[k_][sl], ref_layers[k_][sl]
             assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
 
 
@@ -200,8 +200,8 @@ def _run_sequence(w, P, K, frames):
             for k_ in ("height", "density", "hard", "soft"):
                 a, b = lay[k_][sl], ref_layers[k_][sl]
                 assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
-            for k_ in ("slope", "roughness", "neg"):
-                a, b = lay[k_], ref_layers[k_]
+            for k_ in ("slope", "roughness", "neg"):  # phase 1 is slab-local
+                a, b = lay[k_][sl], ref_layers[k_][sl]
                 assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
 
 
@@ -229,3 +229,79 @@ def _moved(pose, dx):
     p = np.array(pose, dtype=np.float64).reshape(3, 4).copy()
     p[0, 3] += dx
     return p
+
+
+def _run_segments(w, P):
+    """The ray-segment slab partition (gvom_integrate_slab): every rank sees
+    every sensor and traces only the part of each ray inside its rows; its
+    buffer map holds the slab with LOCAL ranks (global = the k of the slabs
+    before + local).  No exchange of counts at all; the surface rows are
+    all-gathered for the plane fits and the cone search as before."""
+    grid = dict(w.grid)
+    grid["buffer_frames"] = 1
+    f = w.frames[0]
+    scans = [(torch.from_numpy(s.points).cuda(), s.pose, s.rings) for s in f.scans]
+    ref = GvomMap(grid, max_points_per_frame=f.n_points)
+    ref.shift(f.vehicle_xyz)
+    ref.integrate_scan(scans)
+    ref.compute_maps()
+    ref_lut, ref_data, _ = ref.export_frame(0)
+    ref_layers = layers_np(ref)
+    nx, ny, nz = ref.nx, ref.ny, ref.nz
+    ys = parallel.slab_rows(ny, P)
+    row = nx * nz
+    ranks = []
+    for r in range(P):
+        m = GvomMap(grid, max_points_per_frame=f.n_points)
+        m.shift(f.vehicle_xyz)
+        m.integrate_slab(scans, ys[r], ys[r + 1])
+        m.compute_maps_slab(ys[r], ys[r + 1], 0)
+        ranks.append(m)
+    surf = torch.cat([ranks[r].surface()[ys[r]:ys[r + 1]] for r in range(P)])
+    for r in range(P):
+        ranks[r].surface().copy_(surf)
+        ranks[r].compute_maps_slab(ys[r], ys[r + 1], 1)
+    torch.cuda.synchronize()
+    base = 0
+    for r in range(P):
+        m = ranks[r]
+        lut, data, _ = m.export_frame(0)
+        k = data["hits"].shape[0]
+        v0, v1 = ys[r] * row, ys[r + 1] * row
+        got = lut[v0:v1].astype(np.int64)
+        got[got >= 0] += base  # local -> global ranks
+        assert np.array_equal(got, ref_lut[v0:v1].astype(np.int64)), f"rank {r} LUT"
+        for k_ in ("hits", "misses", "min_dz", "m1", "m2"):
+            assert np.array_equal(data[k_], ref_data[k_][base:base + k]), (r, k_)
+        base += k
+        lay = layers_np(m)
+        sl = slice(ys[r], ys[r + 1])
+        for k_ in ("height", "density", "hard", "soft"):
+            a, b = lay[k_][sl], ref_layers[k_][sl]
+            assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
+        for k_ in ("slope", "roughness", "neg"):  # phase 1 is slab-local
+            a, b = lay[k_][sl], ref_layers[k_][sl]
+            assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), (r, k_)
+    assert base == ref_data["hits"].shape[0]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_ray_segment_slabs_c4(P):
+    _run_segments(synth.workload(3), P)
+
+
+@pytest.mark.parametrize("P", [8, 16])
+def test_ray_segment_slabs_c1(P):
+    # c1: 64 x 64 x 16 -- a finalize tile holds 8 rows: P = 16 gives 4-row
+    # slabs, so neighbouring slabs share boundary tiles
+    _run_segments(synth.workload(0), P)
+
+
+def test_ray_segment_slabs_c2_and_c3():
+    _run_segments(synth.workload(1), 4)
+    _run_segments(synth.config3(speed=12.0, n_frames=1), 8)
+
+
+@pytest.mark.slow
+def test_ray_segment_slabs_c5_eight_ranks():
+    _run_segments(synth.workload(4), 8)

@@ -165,3 +165,59 @@ def test_slab_rows():
     assert parallel.slab_rows(1024, 8) == [0, 128, 256, 384, 512, 640, 768, 896, 1024]
     with pytest.raises(ValueError):
         parallel.slab_rows(100, 8)
+
+
+def _worker_segments(rank, world, port, q):
+    """The ray-segment partition's exchange: all_gather_scans must hand every
+    rank every sensor (bit-identical points, poses, ring counts, rank order),
+    and global_rank_base must turn the slabs' occupied counts -- here the
+    oracle's, per slab of the two-sensor frame -- into the global ranks of
+    the single-process frame map."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import sys
+        sys.path.insert(0, ROOT)
+        from oracle import oracle as O
+        from paper_2109_13176_b200 import parallel
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        grid, scans = _frame()
+        mine = [(torch.from_numpy(scans[rank][0]), scans[rank][1], 16)]
+        got = parallel.all_gather_scans(mine)
+        assert len(got) == len(scans)
+        for (p, pose, rings), (pr, poser) in zip(got, scans):
+            assert np.array_equal(p.numpy(), pr) and np.array_equal(pose, poser) and rings == 16
+        dims = (grid["nx"], grid["ny"], grid["nz"])
+        nx, ny, nz = dims
+        res = grid["res"]
+        origin = O.snap_origin(nx, ny, nz, res, 0.5, (0.0, 0.0, 0.0))
+        H, M, MN, M1, M2, _ = O.integrate_dense(dims, scans, res, origin)
+        ref = O.frame_map(H, M, MN, M1, M2, origin)
+        ys = parallel.slab_rows(ny, world)
+        v0, v1 = ys[rank] * nx * nz, ys[rank + 1] * nx * nz
+        k_local = int((H[v0:v1] >= 1).sum())
+        base, total = parallel.global_rank_base(torch.tensor(k_local, dtype=torch.int64))
+        assert int(total) == ref.k
+        occ = ref.lut[v0:v1] >= 0
+        if occ.any():  # the slab's first occupied voxel has global rank = base
+            assert int(ref.lut[v0:v1][occ][0]) == int(base)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok", k_local, int(base)))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "fail", traceback.format_exc(), None))
+
+
+def test_segment_exchange_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29400 + (os.getpid() % 200)
+    procs = [ctx.Process(target=_worker_segments, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info, base in res:
+        assert status == "ok", info
