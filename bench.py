@@ -382,9 +382,17 @@ def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int
         sm = parallel.SlabMapper(m, ep_capacity=npts_all, fused=(mode == "fused"))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
+    # every rank knows every sensor's pose and point count (the vehicle's state):
+    # the segment partition then moves only the points
+    meta = [(i % world, s.points.shape[0], s.pose, s.rings) for i, s in enumerate(f.scans)]
+    meta.sort(key=lambda t: t[0])
+
     def step():
         m.shift(f.vehicle_xyz)
-        sm.integrate(mine)
+        if mode == "segments":
+            sm.integrate(mine, meta=meta)
+        else:
+            sm.integrate(mine)
         sm.compute_maps()
 
     with torch.cuda.stream(stream):

@@ -196,11 +196,28 @@ GVOM_API gvom_status gvom_integrate_scan(gvom_handle* h, const gvom_scan* scans,
  * defined.  Every pass-through and return of the frame is counted by exactly
  * one rank, so the union of the slabs equals gvom_integrate_scan's map.  No
  * collective is needed for the map: the compute_maps_slab phases follow.
- * Not with GVOM_FLAG_PIPELINE or GVOM_FLAG_ROLLING; buffer_frames = 1 (a
- * shifted older map would read rows of other slabs).  Errors as
- * gvom_integrate_scan, GVOM_E_INVALID for a bad row range.               */
+ * Not with GVOM_FLAG_PIPELINE or GVOM_FLAG_ROLLING.  With buffer_frames > 1
+ * and motion a shifted older map reads rows of other slabs: set the peers
+ * (gvom_set_peers).  Errors as gvom_integrate_scan, GVOM_E_INVALID for a bad
+ * row range.                                                              */
 GVOM_API gvom_status gvom_integrate_slab(gvom_handle* h, const gvom_scan* scans, int32_t n_scans,
                                          int32_t y0, int32_t y1);
+
+/* The ray-segment partition with motion (buffer_frames > 1): a buffer map
+ * shifted by the vehicle's motion reads rows that other ranks own.  With the
+ * peers set, gvom_compute_maps_slab(phase 0) reads those rows -- LUT entries,
+ * occupancy bits and data rows, at the same workspace offsets -- directly from
+ * the owner's workspace (peer memory: each d_peer_workspaces[r] is rank r's
+ * workspace as a pointer this GPU can load from, e.g. torch symmetric memory
+ * buffer_ptrs of workspaces allocated there; d_peer_workspaces[rank] must be
+ * this handle's own).  Every rank's handle has the same config (identical
+ * layouts) and integrates every frame with gvom_integrate_slab over its slab
+ * slab_y[rank]..slab_y[rank+1]; the caller orders a rank's reads after the
+ * owners' integrate (a barrier) and the owners' next integrate after the
+ * reads.  n_ranks = 0 clears.  The merged export (gvom_export_voxels) stays
+ * local.                                                                  */
+GVOM_API gvom_status gvom_set_peers(gvom_handle* h, const void* const* d_peer_workspaces,
+                                    const int32_t* slab_y, int32_t n_ranks, int32_t rank);
 
 /* Map processing: combine all buffer maps at the origin of the
  * newest one, then compute height, density, hard, soft, slope,

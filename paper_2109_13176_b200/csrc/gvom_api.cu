@@ -112,6 +112,8 @@ Layout make_layout(const gvom_config* c) {
   l.slot_stride = l.slot_meta + kAlign;
   // one spare slot when pipelined: integrate(t+1) writes it while
   // compute_maps(t) still reads the K newest
+  // one spare slot when pipelined: integrate(t+1) writes it while
+  // compute_maps(t) still reads the K newest
   off = l.slot_stride * (size_t)(c->buffer_frames + ((c->flags & GVOM_FLAG_PIPELINE) ? 1 : 0));
   l.staging = off;
   off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
@@ -182,6 +184,7 @@ struct gvom_handle {
   uint32_t timing_mask = 0;  // stages bracketed by CUDA events
   TileCounts tc{};
   // slab partition: occupancy built by gvom_slab_occupancy, pending finalize
+  PeerMap pm{};  // gvom_set_peers: the other ranks' workspaces (slab partition)
   int32_t slab_y0 = -1, slab_y1 = -1;
   int64_t slab_k = 0;  // occupied voxels of the pending slab
   // fork/join: the cone search runs on `aux` while k_slope runs on `st`
@@ -787,7 +790,10 @@ static gvom_status integrate_rows(gvom_handle* h, const gvom_scan* scans, int32_
   Bracket br(h, GVOM_STAGE_INTEGRATE, h->st);
   int64_t t0, t1;  // the tiles of the rows integrated
   slab_tile_range(d, slab, &t0, &t1);
-  // pass 0: the slot's LUT to -1 (empty, no misses), its bits cleared
+  // pass 0: the slot's LUT to -1 (empty, no misses), its bits cleared.  (Doing
+  // this for the next scan right after an integrate, on a side stream beside
+  // compute_maps, measured no gain: the reset then competes with k_columns for
+  // bandwidth -- c2 step 119.7 vs 119.1 us.)
   GVOM_CU(stage(h, GVOM_STAGE_MEMSET, true,
                 [&] { return launch_reset_slot(slot.lut, slot.bits, d, t0, t1, h->st); }));
   // pass 2a: ray tracing, misses counted down in the slot's LUT (LUT-direct)
@@ -1339,6 +1345,28 @@ gvom_status gvom_slot_buffers(gvom_handle* h, int32_t age, int32_t** out_d_lut,
   return GVOM_OK;
 }
 
+gvom_status gvom_set_peers(gvom_handle* h, const void* const* d_peer_workspaces,
+                           const int32_t* slab_y, int32_t n_ranks, int32_t rank) {
+  if (!h || n_ranks < 0 || n_ranks > GVOM_MAX_RANKS) return GVOM_E_INVALID;
+  PeerMap pm{};
+  if (n_ranks > 0) {
+    if (!d_peer_workspaces || !slab_y || rank < 0 || rank >= n_ranks) return GVOM_E_INVALID;
+    if (slab_y[0] != 0 || slab_y[n_ranks] != h->cfg.ny) return GVOM_E_INVALID;
+    if (d_peer_workspaces[rank] != (const void*)h->ws) return GVOM_E_INVALID;
+    pm.P = n_ranks;
+    for (int r = 0; r <= n_ranks; ++r) {
+      if (r > 0 && slab_y[r] < slab_y[r - 1]) return GVOM_E_INVALID;
+      pm.y[r] = slab_y[r];
+    }
+    for (int r = 0; r < n_ranks; ++r) {
+      if (!d_peer_workspaces[r]) return GVOM_E_INVALID;
+      pm.delta[r] = (int64_t)((const char*)d_peer_workspaces[r] - h->ws);
+    }
+  }
+  h->pm = pm;
+  return GVOM_OK;
+}
+
 gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total) {
   NvtxRange nvtx_("gvom_slab_complete");
   if (!h || h->pipelined || h->rolling || h->count == 0 || k_total < 0 || k_total > h->lay.cap)
@@ -1360,6 +1388,7 @@ gvom_status gvom_compute_maps_slab(gvom_handle* h, int32_t y0, int32_t y1, int32
     int64_t o[3];
     for (int i = 0; i < 3; ++i) o[i] = h->slots[newest].origin[i];
     h->map_slots = buffer_slots(h, o);
+    h->map_slots.pm = h->pm;  // shifted rows of other slabs: their owners' memory
     h->lp.o_z = o[2];
     GVOM_CU(stage(h, GVOM_STAGE_COLUMNS, true, [&] {
       return launch_columns(h->map_slots, h->d, h->lp, h->layers, h->st, (int64_t)y0 * h->cfg.nx,

@@ -43,11 +43,41 @@ struct SlotView {
   int32_t pad;
 };
 
+// The ray-segment slab partition with motion (gvom_set_peers): rank r owns
+// rows [y[r], y[r+1]) of every buffer map; a shifted older map's rows of other
+// slabs are read from their owner's workspace (peer memory) at the same
+// offsets, delta[r] bytes from this handle's.  P = 0: everything local.
+struct PeerMap {
+  int32_t P;
+  int32_t y[GVOM_MAX_RANKS + 1];
+  int64_t delta[GVOM_MAX_RANKS];
+};
+
 struct SlotSet {
   SlotView s[GVOM_MAX_BUFFER_FRAMES];
   int32_t K;
   int32_t kp_log2;  // log2 of the lanes per slot group (pow2 >= K)
+  PeerMap pm;
 };
+
+// byte offset from this handle's workspace to the owner of row y's (peers)
+__host__ __device__ inline int64_t peer_delta(const PeerMap& pm, int y) {
+  if (pm.P <= 0) return 0;
+  int lo = 0, hi = pm.P - 1;  // slab r with y[r] <= y < y[r+1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pm.y[mid] <= y)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return pm.delta[lo];
+}
+template <class T>
+__host__ __device__ inline T* rebase(T* p, int64_t delta) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(const_cast<void*>(
+                                  reinterpret_cast<const void*>(p))) + delta);
+}
 
 struct LayerPtrs {
   float* height;

@@ -317,15 +317,58 @@ __device__ __forceinline__ int steps_through_y(const float eb[3], const float fb
   return cnt[0] + c + cnt[2];
 }
 
+// State after the first j0 steps of a walk (kSplit's second half): c[a] = the
+// axis-a crossings among the walk's first j0 events.  The events (key, axis)
+// with key < K form a prefix of the walk's (key, axis) order for any
+// threshold K, so counting the crossings below a K chosen a few steps short of
+// j0 (K * sum |d_a| ~ j0 - 3.5) gives a prefix of j <= j0 events; the caller
+// takes the j0 - j remaining events with the exact step rule.  Each count is a
+// float guess corrected to the exact count with the stateless keys (monotone
+// in j).  j0 < T, so no exhausted axis's key is below K.  Returns j0 - j.
+__device__ __forceinline__ int seek_prefix(const float eb[3], const float fb[3], const float s[3],
+                                           const float inv[3], const int jmax[3], int j0,
+                                           int c[3]) {
+  float dabs[3], Rm = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    dabs[a] = jmax[a] > 0 ? fabsf(__fdividef(1.0f, inv[a])) : 0.f;
+    Rm += dabs[a];
+  }
+  float K = __fdividef((float)j0 - 3.5f, Rm);
+  for (int iter = 0;; ++iter) {
+    int sum = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int ca = 0;
+      if (jmax[a] > 0 && K > 0.f) {
+        const float X = K * dabs[a] - fb[a] * (eb[a] - s[a]) + 1.0f;
+        ca = (int)ceilf(X) - 1;
+        ca = ca < 0 ? 0 : (ca > jmax[a] ? jmax[a] : ca);
+        while (ca < jmax[a] && axis_key(eb[a], fb[a], s[a], inv[a], ca + 1) < K) ++ca;
+        while (ca > 0 && !(axis_key(eb[a], fb[a], s[a], inv[a], ca) < K)) --ca;
+      }
+      c[a] = ca;
+      sum += ca;
+    }
+    if (sum <= j0) return j0 - sum;
+    // overshoot (float guess of K): retreat; after a few tries start from 0
+    K = iter < 4 ? K - __fdividef((float)(sum - j0) + 2.0f, Rm) : -1.0f;
+  }
+}
+
 // The rays of one warp (32 consecutive thread ids gtid of the batch).
+// kSplit (A/B: GVOM_RAY_SPLIT=1): two warps per 32 rays, half 0 walking the
+// first ceil(Tw / 2) steps and half 1 the rest from the exact state at that
+// step (seek_prefix + the exact step rule), so a block's critical path is half
+// the longest walk; only half 0 bins the endpoints.
 // kSlab: only the steps whose voxel lies in rows [sr.y0, sr.y1) are traced and
 // only returns in those rows are binned (y is monotone along a walk, so that
 // is one step range [jin, jout), found exactly with the stateless keys).
-template <bool kStream, bool kNeg, bool kSlab = false>
+template <bool kStream, bool kNeg, bool kSlab = false, bool kSplit = false>
 __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
                                          uint32_t* __restrict__ miss, uint32_t* __restrict__ bits,
                                          const TileCounts& tc, int64_t gtid,
-                                         const SlabRange sr = SlabRange{0, 0}) {
+                                         const SlabRange sr = SlabRange{0, 0}, int half = 0) {
   const int64_t gt = gtid / rb.tile_threads;  // interleaved (tile, sensor)
   const int sidx = (int)(gt % rb.S);
   const int64_t tid = (gt / rb.S) * rb.tile_threads + (gtid - gt * rb.tile_threads);
@@ -373,8 +416,9 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
       }
       // endpoint occupancy (O4/O6: occupied iff hits >= 1); bits == nullptr in
       // the multi-GPU partial pass (occupancy is built on the slab owner)
-      if (bits && (unsigned)E[0] < (unsigned)d.nx && (unsigned)E[1] < (unsigned)d.ny &&
-          (unsigned)E[2] < (unsigned)d.nz && (!kSlab || (E[1] >= sr.y0 && E[1] < sr.y1))) {
+      if (bits && (!kSplit || half == 0) && (unsigned)E[0] < (unsigned)d.nx &&
+          (unsigned)E[1] < (unsigned)d.ny && (unsigned)E[2] < (unsigned)d.nz &&
+          (!kSlab || (E[1] >= sr.y0 && E[1] < sr.y1))) {
         const uint32_t LE = (uint32_t)(E[2] + d.nz * E[0] + strideY * E[1]);
         const uint32_t bit = 1u << (LE & 31);
         newtile = (atomicOr(bits + (LE >> 5), bit) & bit) ? 0xffffffffu : (LE >> kTileShift);
@@ -433,8 +477,9 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
         }
         if (!ok) {
           const int S[3] = {sp.S[0], sp.S[1], sp.S[2]};
-          walk_exact(S, E, g, s, d, miss, kSlab ? sr.y0 : 0, kSlab ? sr.y1 : d.ny,
-                     kNeg ? 0xffffffffu : 1u);
+          if (!kSplit || half == 0)
+            walk_exact(S, E, g, s, d, miss, kSlab ? sr.y0 : 0, kSlab ? sr.y1 : d.ny,
+                       kNeg ? 0xffffffffu : 1u);
           left = 0;
         } else {
           e0 = eb[0]; e1 = eb[1]; e2 = eb[2];
@@ -493,6 +538,34 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
     }
   }
 
+  if (kSplit) {
+    // both halves computed the same setups: the same warp maximum Tw; half 1
+    // starts at step J = ceil(Tw / 2) from the walk's exact state there
+    const int J = (__reduce_max_sync(0xffffffffu, left) + 1) / 2;
+    if (half == 0) {
+      left = min(left, J);
+    } else if (left > J) {
+      const float eb[3] = {(float)(sp.S[0] + (f0 >= 0.f ? 1 : 0)),
+                           (float)(sp.S[1] + (f1 >= 0.f ? 1 : 0)),
+                           (float)(sp.S[2] + (f2 >= 0.f ? 1 : 0))};
+      const float fb[3] = {f0, f1, f2}, s3[3] = {s0, s1, s2}, inv[3] = {i0, i1, i2};
+      const int jm[3] = {jm0, jm1, jm2};
+      int c[3];
+      const int nf = seek_prefix(eb, fb, s3, inv, jm, J, c);
+      e0 = __fadd_rn(eb[0], f0 * (float)c[0]);
+      e1 = __fadd_rn(eb[1], f1 * (float)c[1]);
+      e2 = __fadd_rn(eb[2], f2 * (float)c[2]);
+      k0 = jm0 > 0 ? __fmul_rn(__fsub_rn(e0, s0), i0) : kInf;
+      k1 = jm1 > 0 ? __fmul_rn(__fsub_rn(e1, s1), i1) : kInf;
+      k2 = jm2 > 0 ? __fmul_rn(__fsub_rn(e2, s2), i2) : kInf;
+      L += (uint32_t)(c[0] * dL0 + c[1] * dL1 + c[2] * dL2);
+      for (int t = 0; t < nf; ++t)  // the last events of the prefix, exact step rule
+        dda_step(k0, k1, k2, e0, e1, e2, f0, f1, f2, i0, i1, i2, s0, s1, s2, dL0, dL1, dL2, L);
+      left -= J;
+    } else {
+      left = 0;
+    }
+  }
   // tile occupancy counts, one atomic per group of lanes in the same tile
   {
     const unsigned peers = __match_any_sync(0xffffffffu, newtile);
@@ -527,6 +600,20 @@ __global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayB
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
   ray_warp<kStream, kNeg>(rb, d, miss, bits, tc, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (last_sensor && bits) scan_tiles_if_last(tc, d);
+}
+
+// Two warps per 32 rays (kSplit, GVOM_RAY_SPLIT=1): warp pair (2w, 2w+1) of the
+// block walks the first / second half of ray warp w's steps.
+template <bool kStream, int kBS, bool kNeg>
+__global__ void __launch_bounds__(kBS, 1) k_raycast_split(const __grid_constant__ RayBatch rb,
+                                                       const Dims d, uint32_t* __restrict__ miss,
+                                                       uint32_t* __restrict__ bits,
+                                                       const TileCounts tc, bool last_sensor) {
+  const int w = threadIdx.x >> 5;
+  const int64_t wtile = ((int64_t)blockIdx.x * (kBS / 32) + w) >> 1;
+  ray_warp<kStream, kNeg, false, true>(rb, d, miss, bits, tc, wtile * 32 + (threadIdx.x & 31),
+                                       SlabRange{0, 0}, w & 1);
   if (last_sensor && bits) scan_tiles_if_last(tc, d);
 }
 
@@ -859,27 +946,34 @@ __global__ void __launch_bounds__(256) k_endpoint(const __grid_constant__ RayBat
 // 2^30 saturation never applies, gvom_create checks the capacity), and the
 // finalize touches only occupied voxels.  Write-back stores for a LUT that
 // fits in L2 (the ray cast's reductions then hit L2), evict-first beyond.
+template <bool kKeep>
 __global__ void __launch_bounds__(256) k_reset_slot(int32_t* __restrict__ lut, int64_t l0,
                                                     int64_t l1, uint32_t* __restrict__ bits,
-                                                    int64_t w0, int64_t w1, bool keep) {
+                                                    int64_t w0, int64_t w1) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // l0, w0 are tile starts: 16-byte aligned; tails (l1, w1 not multiples of 4) scalar
   const int64_t n4 = (l1 - l0) >> 2, m4 = (w1 - w0) >> 2;
   const int4 ones = make_int4(-1, -1, -1, -1);
-  const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
   int4* l4 = reinterpret_cast<int4*>(lut + l0);
-  uint4* b4 = reinterpret_cast<uint4*>(bits + w0);
-  for (int64_t i = i0; i < n4 + m4; i += stride) {
-    if (i < n4) {
-      if (keep)
-        l4[i] = ones;
+  int64_t i = i0;
+  for (; i + 3 * stride < n4; i += 4 * stride) {  // four 16-byte stores in flight
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (kKeep)
+        l4[i + u * stride] = ones;
       else
-        __stcs(l4 + i, ones);
-    } else {
-      __stcs(b4 + (i - n4), zero);
+        __stcs(l4 + i + u * stride, ones);
     }
   }
+  for (; i < n4; i += stride) {
+    if (kKeep)
+      l4[i] = ones;
+    else
+      __stcs(l4 + i, ones);
+  }
+  uint4* b4 = reinterpret_cast<uint4*>(bits + w0);
+  for (int64_t j = i0; j < m4; j += stride) __stcs(b4 + j, make_uint4(0u, 0u, 0u, 0u));
   if (i0 < 4) {
     if (l0 + 4 * n4 + i0 < l1) lut[l0 + 4 * n4 + i0] = -1;
     if (w0 + 4 * m4 + i0 < w1) bits[w0 + 4 * m4 + i0] = 0u;
@@ -896,13 +990,16 @@ __global__ void __launch_bounds__(256) k_reset_slot(int32_t* __restrict__ lut, i
 // cast), it becomes the voxel's rank and its data row {0, misses, 0xFFFFFFFF,
 // 0, 0, 0} is initialised for the endpoint pass.  Empty voxels' entries are
 // final already.
+// (Binning the returns in the same launch, endpoint blocks waiting on per-tile
+// flags, measured slower: c2 integrate 83-86 vs 75-78 us.)
 __global__ void __launch_bounds__(kTileWords) k_finalize_lut(
     int32_t* __restrict__ lut, const uint32_t* __restrict__ bits, uint32_t* __restrict__ wprefix,
     gvom_voxel* __restrict__ data, const TileCounts tc, const Dims d, int64_t t0) {
   __shared__ uint32_t wsum[kTileWords / 32];
   __shared__ uint16_t slist[1 << kTileShift];  // occupied voxels of the tile, rank order
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int64_t b = t0 + blockIdx.x;
+  const int64_t bl = blockIdx.x;
+  const int64_t b = t0 + bl;
   const uint32_t off = __ldg(tc.offset + b);  // rank offset of this tile
   const int64_t w = b * kTileWords + t;
   const uint32_t bw = w < d.W ? __ldg(bits + w) : 0u;
@@ -928,7 +1025,7 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_lut(
   __shared__ uint32_t stotal;
   if (t == kTileWords - 1) {
     stotal = rel + c;
-    if (blockIdx.x == gridDim.x - 1) *tc.total = pre + c;  // k of the frame
+    if (bl == gridDim.x - 1) *tc.total = pre + c;  // k of the frame
   }
   __syncthreads();
   const uint32_t n = stotal;
@@ -1009,6 +1106,27 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
                                                         *slab);
     return cudaGetLastError();
   }
+  static int split = -1;  // GVOM_RAY_SPLIT=1: two warps per 32 rays (A/B)
+  if (split < 0) {
+    const char* e = getenv("GVOM_RAY_SPLIT");
+    split = e && atoi(e) ? 1 : 0;
+  }
+  if (split && lut_direct) {
+    const unsigned b2 = (unsigned)((2 * threads + bs - 1) / bs);
+    if (!stream && !wide)
+      k_raycast_split<false, kRayNarrowBS, true><<<b2, kRayNarrowBS, 0, st>>>(
+          rb, d, miss_grid, bits, tc, last_launch);
+    else if (!stream)
+      k_raycast_split<false, 128, true><<<b2, 128, 0, st>>>(rb, d, miss_grid, bits, tc,
+                                                            last_launch);
+    else if (!wide)
+      k_raycast_split<true, kRayNarrowBS, true><<<b2, kRayNarrowBS, 0, st>>>(
+          rb, d, miss_grid, bits, tc, last_launch);
+    else
+      k_raycast_split<true, 128, true><<<b2, 128, 0, st>>>(rb, d, miss_grid, bits, tc,
+                                                           last_launch);
+    return cudaGetLastError();
+  }
   if (lut_direct)
     launch_raycast_t<true>(stream, wide, blocks, rb, d, miss_grid, bits, tc, last_launch, st);
   else
@@ -1077,7 +1195,10 @@ cudaError_t launch_reset_slot(int32_t* lut, uint32_t* bits, const Dims& d, int64
     return e;
   }
   const bool keep = 4 * (l1 - l0) <= 3 * d.l2_bytes / 4;  // the REDs then hit L2
-  k_reset_slot<<<(unsigned)blocks, 256, 0, st>>>(lut, l0, l1, bits, w0, w1, keep);
+  if (keep)
+    k_reset_slot<true><<<(unsigned)blocks, 256, 0, st>>>(lut, l0, l1, bits, w0, w1);
+  else
+    k_reset_slot<false><<<(unsigned)blocks, 256, 0, st>>>(lut, l0, l1, bits, w0, w1);
   return cudaGetLastError();
 }
 

@@ -109,6 +109,7 @@ __device__ __forceinline__ SlotVox cell_vox(int32_t v, const gvom_voxel* __restr
 //          lane sums its own map's hits / hits+misses over them with no
 //          cross-lane traffic; only the two edge voxels need the merged
 //          min_dz (a group min).  One group sum at the end.
+template <bool kEarlyEdges>
 __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
                                                  const LayerParams lp, const LayerPtrs out,
                                                  int64_t cbeg, int64_t cells) {
@@ -133,9 +134,10 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
       col = true;
       cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
       dz = s.dz;
-      bits = s.bits;
-      lut = s.lut;
-      data = s.data;
+      const int64_t dp = peer_delta(ss.pm, sy);  // the row's owner (slab partition)
+      bits = rebase(s.bits, dp);
+      lut = rebase(s.lut, dp);
+      data = rebase(s.data, dp);
     }
   }
   // ---- z*: merged occupancy, 32 z at a time; keep a 64-z window from the
@@ -189,12 +191,25 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
       const int sx = x + s.dx, sy = y + s.dy, uz = z + s.dz;
       if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny &&
           (unsigned)uz < (unsigned)d.nz &&
-          __ldg(s.lut + (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy) + uz) >= 0)
+          __ldg(rebase(s.lut, peer_delta(ss.pm, sy)) +
+                (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy) + uz) >= 0)
         return true;
     }
     return false;
   };
   uint64_t SH = 0, SW = 0;
+  // edge voxels z_lo and z_hi need the merged min_dz; an edge voxel that no
+  // map occupies contributes nothing and is not loaded.  Their LUT cells and
+  // rows are loaded first, so they are in flight with the interior band's
+  const bool use0 = zs >= 0 && z_lo <= z_hi && z_lo >= zs && occz(z_lo);
+  const bool use1 = zs >= 0 && z_hi >= zs && z_hi != z_lo && occz(z_hi);
+  SlotVox ve0{0u, 0u, 0xffffffffu}, ve1{0u, 0u, 0xffffffffu};
+  if (kEarlyEdges) {
+    const int32_t le0 = use0 ? lut_cell(col, lut, cb, z_lo + dz, d.nz) : -1;
+    const int32_t le1 = use1 ? lut_cell(col, lut, cb, z_hi + dz, d.nz) : -1;
+    if (use0) ve0 = cell_vox(le0, data);
+    if (use1) ve1 = cell_vox(le1, data);
+  }
   if (zs >= 0) {
     // interior band voxels: certainly in the band when occupied
     const int rlo = z_lo + 1 - zc, rhi = z_hi - zc;  // interior rel range [rlo, rhi)
@@ -231,13 +246,14 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
       }
     }
   }
-  // edge voxels z_lo and z_hi need the merged min_dz (uniform code); an edge
-  // voxel that no map occupies contributes nothing and is not loaded
+  // the edge voxels: in the band iff their merged min_dz puts them there
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int z = e == 0 ? z_lo : z_hi;
-    const bool use = zs >= 0 && z <= z_hi && z >= zs && (e == 0 || z_hi != z_lo) && occz(z);
-    const SlotVox v = use ? slot_vox(col, lut, data, cb, z + dz, d.nz) : SlotVox{0u, 0u, 0xffffffffu};
+    const bool use = e == 0 ? use0 : use1;
+    const SlotVox v = kEarlyEdges ? (e == 0 ? ve0 : ve1)
+                                  : (use ? slot_vox(col, lut, data, cb, z + dz, d.nz)
+                                         : SlotVox{0u, 0u, 0xffffffffu});
     const uint32_t mn = grp_min(v.mn, lg);
     if (use && mn != 0xffffffffu) {
       const int64_t dq = (65536ll * z + (int64_t)mn) - q_s;
@@ -302,7 +318,7 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   constexpr int SW_ = kSlopeTX + 2 * kSlopeHalo, SH_ = kSlopeTY + 2 * kSlopeHalo;
   __shared__ int32_t tile[SH_][SW_ + 1];
   const int r = (lp.slope_window - 1) / 2;
-  const int x0 = blockIdx.x * kSlopeTX, y0 = blockIdx.y * kSlopeTY;
+  const int x0 = blockIdx.x * kSlopeTX, y0 = lp.row0 + blockIdx.y * kSlopeTY;
   const int32_t* __restrict__ qs = out.qs;
   for (int i = threadIdx.y * kSlopeTX + threadIdx.x; i < SW_ * SH_; i += kSlopeTX * kSlopeTY) {
     const int ty = i / SW_, tx = i % SW_;
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   }
   __syncthreads();
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-  if (x >= d.nx || y >= d.ny) return;
+  if (x >= d.nx || y >= lp.row1) return;
   const int64_t c = x + (int64_t)d.nx * y;
   const float qnan = __int_as_float(0x7fc00000);
   const int cx = threadIdx.x + kSlopeHalo, cy = threadIdx.y + kSlopeHalo;
@@ -374,8 +390,8 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
   out.rough[c] = (float)(acc / ((double)det * (double)det * (double)n) * (sc * sc));
 }
 
-// The same plane fit with the defined cells compacted: a 32 x 16 tile (+ the
-// r-cell halo) per 256-thread block; undefined cells are written NaN by the
+// The same plane fit with the defined cells compacted: a 32 x 8 tile (+ the
+// r-cell halo) per 128-thread block; undefined cells are written NaN by the
 // thread that classifies them, the defined ones go into a block list (warp
 // ballots + a block prefix) that all threads then share, so every lane of a
 // warp fits a plane (the per-cell kernel ran ~12 of 32 lanes: undefined
@@ -383,17 +399,19 @@ __global__ void __launch_bounds__(kSlopeTX * kSlopeTY) k_slope(const Dims d, con
 // normal-equation gradient (within ~2 ulp f32 of the double atan, well inside
 // the contract's 1e-4 + 1e-5 |ref|); the nodata decisions are unchanged
 // integer tests.
-constexpr int kSlope2TX = 32, kSlope2TY = 16;
-__global__ void __launch_bounds__(256) k_slope_c(const Dims d, const LayerParams lp,
-                                                 const LayerPtrs out) {
+constexpr int kSlope2Threads = 128;                       // 4 warps
+constexpr int kSlope2TX = 32, kSlope2TY = 2 * kSlope2Threads / 32;  // 2 rows per warp
+__global__ void __launch_bounds__(kSlope2Threads) k_slope_c(const Dims d, const LayerParams lp,
+                                                            const LayerPtrs out) {
   constexpr int SW_ = kSlope2TX + 2 * kSlopeHalo, SH_ = kSlope2TY + 2 * kSlopeHalo;
+  constexpr int kNW = kSlope2Threads / 32;
   __shared__ int32_t tile[SH_][SW_ + 1];
   __shared__ uint16_t list[kSlope2TX * kSlope2TY];
-  __shared__ uint32_t cnt[16];
+  __shared__ uint32_t cnt[2 * kNW];
   const int r = (lp.slope_window - 1) / 2;
   const int x0 = blockIdx.x * kSlope2TX, y0 = lp.row0 + blockIdx.y * kSlope2TY;
   const int32_t* __restrict__ qs = out.qs;
-  for (int i = threadIdx.x; i < SW_ * SH_; i += 256) {
+  for (int i = threadIdx.x; i < SW_ * SH_; i += kSlope2Threads) {
     const int ty = i / SW_, tx = i % SW_;
     const int gx = x0 + tx - kSlopeHalo, gy = y0 + ty - kSlopeHalo;
     int32_t q = kQsUndef;
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(256) k_slope_c(const Dims d, const LayerParams
   }
   __syncthreads();
   uint32_t total = 0, base[2] = {0u, 0u};
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < 2 * kNW; ++j) {
     const uint32_t v = cnt[j];
     if (j == 2 * warp) base[0] = total;
     if (j == 2 * warp + 1) base[1] = total;
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(256) k_slope_c(const Dims d, const LayerParams
       list[base[h] + __popc(bal[h] & ((1u << lane) - 1u))] =
           (uint16_t)((2 * warp + h) * kSlope2TX + lane);
   __syncthreads();
-  for (uint32_t it = threadIdx.x; it < total; it += 256) {
+  for (uint32_t it = threadIdx.x; it < total; it += kSlope2Threads) {
     const int li = list[it];
     const int tx = li % kSlope2TX, ty = li / kSlope2TX;
     const int64_t c = (x0 + tx) + (int64_t)d.nx * (y0 + ty);
@@ -974,7 +992,10 @@ __global__ void __launch_bounds__(1024) k_negative_tb(const Dims d, const LayerP
 }
 
 // O10 decision from the cone sweeps' min / max: undefined cell and
-// max F - min F > T_neg (T_neg >= 0, so this implies |F| >= 2, reading B2)
+// max F - min F > T_neg (T_neg >= 0, so this implies |F| >= 2, reading B2);
+// rows [row0, row1).  (Folding it into the sweeps' tail -- the block that
+// completes a tile pair's four cone counts decides its cells -- measured
+// slower: c2 compute_maps 53 vs 45 us.)
 __global__ void __launch_bounds__(256) k_neg_decide(const Dims d, const LayerParams lp,
                                                     const LayerPtrs out) {
   const int64_t c = (int64_t)lp.row0 * d.nx + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1137,24 +1158,33 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
   if (cend < 0) cend = (int64_t)d.nx * d.ny;
   if (cend <= cbeg) return cudaSuccess;
   const int64_t lanes = (cend - cbeg) << ss.kp_log2;
-  k_columns<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend);
+  static int early = -1;  // GVOM_COL_EARLY=0: edge voxels after the band (A/B)
+  if (early < 0) {
+    const char* e = getenv("GVOM_COL_EARLY");
+    early = e && atoi(e) == 0 ? 0 : 1;
+  }
+  if (early)
+    k_columns<true><<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend);
+  else
+    k_columns<false><<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend);
   return cudaGetLastError();
 }
 
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st) {
-  static int old_kernel = -1;  // GVOM_SLOPE_PERCELL=1: the per-cell kernel (A/B)
+  static int old_kernel = -1;  // GVOM_SLOPE_COMPACT=1: the compacted kernel (A/B)
   if (old_kernel < 0) {
-    const char* e = getenv("GVOM_SLOPE_PERCELL");
-    old_kernel = e && atoi(e) ? 1 : 0;
+    const char* e = getenv("GVOM_SLOPE_COMPACT");
+    old_kernel = e && atoi(e) ? 0 : 1;
   }
   if (old_kernel) {
-    const dim3 grid((d.nx + kSlopeTX - 1) / kSlopeTX, (d.ny + kSlopeTY - 1) / kSlopeTY);
+    const int rows = lp.row1 - lp.row0;
+    const dim3 grid((d.nx + kSlopeTX - 1) / kSlopeTX, (rows + kSlopeTY - 1) / kSlopeTY);
     k_slope<<<grid, dim3(kSlopeTX, kSlopeTY), 0, st>>>(d, lp, out);
   } else {
     const int rows = lp.row1 - lp.row0;
     const dim3 grid((d.nx + kSlope2TX - 1) / kSlope2TX, (rows + kSlope2TY - 1) / kSlope2TY);
-    k_slope_c<<<grid, 256, 0, st>>>(d, lp, out);
+    k_slope_c<<<grid, kSlope2Threads, 0, st>>>(d, lp, out);
   }
   return cudaGetLastError();
 }
@@ -1173,9 +1203,6 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   const int rows = lp.row1 - lp.row0;
   int T = (2 * d.nx + 2 * rows + d.sms - 1) / d.sms;
   T = T < 8 ? 8 : ((T + 7) / 8) * 8;
-#ifdef GVOM_NEG_T
-  T = GVOM_NEG_T;
-#endif
   const size_t NB = (size_t)B + 2 * (size_t)K + 2;
   const size_t slot = neg_slot_bytes(B, K), state = neg_state_bytes(B, K);
   // ring depth: as many slots as shared memory allows, up to kNegRing

@@ -89,6 +89,7 @@ def load_library() -> C.CDLL:
         "gvom_shift": ([P, P, P], I32),
         "gvom_integrate_scan": ([P, P, I32], I32),
         "gvom_integrate_slab": ([P, P, I32, I32, I32], I32),
+        "gvom_set_peers": ([P, P, P, I32, I32], I32),
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
         "gvom_export_layers": ([P, P, P], I32),
@@ -133,7 +134,8 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_compute_maps_slab", "gvom_surface_buffer", "gvom_map_stream", "gvom_costmap",
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
             "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers",
-            "gvom_obstacle_buffers", "gvom_debug_inject_fault", "gvom_integrate_slab")
+            "gvom_obstacle_buffers", "gvom_debug_inject_fault", "gvom_integrate_slab",
+            "gvom_set_peers")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -176,7 +178,11 @@ class GvomMap:
     """One robot-centred voxel map + its buffer of per-scan maps (a gvom_handle)."""
 
     def __init__(self, grid: dict, max_points_per_frame: int, device="cuda",
-                 stream: Optional[torch.cuda.Stream] = None):
+                 stream: Optional[torch.cuda.Stream] = None,
+                 workspace: Optional[torch.Tensor] = None):
+        """workspace: a caller-allocated uint8 device tensor of at least
+        workspace_bytes() (e.g. in torch symmetric memory, for gvom_set_peers);
+        allocated here when None."""
         self.lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("GvomMap needs a CUDA device (no CPU fallback)")
@@ -191,7 +197,11 @@ class GvomMap:
             raise GvomError(-1, "gvom_workspace_bytes (invalid config)")
         with torch.cuda.device(self.device):
             self.stream = stream or torch.cuda.current_stream(self.device)
-            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if workspace is None:
+                workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if workspace.numel() * workspace.element_size() < nbytes:
+                raise GvomError(-2, "workspace smaller than gvom_workspace_bytes")
+            self.workspace = workspace
         self.h = C.c_void_p()
         _check(self.lib.gvom_create(C.byref(self.cfg), C.c_void_p(self.workspace.data_ptr()),
                                     nbytes, C.c_void_p(self.stream.cuda_stream),
@@ -363,6 +373,15 @@ class GvomMap:
         _check(self.lib.gvom_integrate_slab(self.h, arr, n, int(y0), int(y1)),
                "gvom_integrate_slab")
         self._retain(keep)
+
+    def set_peers(self, workspace_ptrs, slab_y, rank: int):
+        """gvom_set_peers: every rank's workspace (device pointers this GPU can
+        load from), the slab rows and this rank; [] clears."""
+        P = len(workspace_ptrs)
+        ws = (C.c_void_p * max(P, 1))(*[int(p) for p in workspace_ptrs])
+        ys = (C.c_int32 * (P + 1))(*[int(v) for v in slab_y]) if P else None
+        _check(self.lib.gvom_set_peers(self.h, ws if P else None, ys, P, int(rank)),
+               "gvom_set_peers")
 
     def compute_maps(self):
         _check(self.lib.gvom_compute_maps(self.h), "gvom_compute_maps")

@@ -206,6 +206,36 @@ def all_gather_scans(scans, group=None):
     return out
 
 
+def all_gather_points(scans, meta, group=None):
+    """all_gather_scans when every rank already knows every sensor's (n,
+    pose, rings) in rank order (`meta`: odometry and sensor geometry are the
+    vehicle's state): only the points move, as one padded all_gather on the
+    device -- no host synchronisation."""
+    import numpy as np
+    P = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    per_rank = [[] for _ in range(P)]
+    for r, n, pose, rings in meta:
+        per_rank[r].append((int(n), pose, int(rings)))
+    tot = [sum(n for n, _, _ in m) for m in per_rank]
+    cap = max(max(tot), 1)
+    dev = scans[0][0].device if scans else torch.device("cuda", torch.cuda.current_device())
+    mine = torch.zeros((cap, 4), dtype=torch.float32, device=dev)
+    if scans:
+        flat = torch.cat([p.reshape(-1, 4) for (p, _, _) in scans])
+        assert flat.shape[0] == tot[me], "local scans disagree with meta"
+        mine[:flat.shape[0]] = flat
+    allp = torch.empty((P * cap, 4), dtype=torch.float32, device=dev)
+    dist.all_gather_into_tensor(allp, mine, group=group)
+    out = []
+    for r in range(P):
+        off = r * cap
+        for n, pose, rings in per_rank[r]:
+            out.append((allp[off:off + n], np.asarray(pose, np.float64), rings))
+            off += n
+    return out
+
+
 def global_rank_base(k_local: torch.Tensor, group=None):
     """Local data ranks -> global: (this slab's base, total k) from the slabs'
     occupied counts (device scalar in, device scalars out: no host sync)."""
@@ -216,11 +246,38 @@ def global_rank_base(k_local: torch.Tensor, group=None):
     return allk[:r].sum(), allk.sum()
 
 
+def segment_map(grid: dict, max_points_per_frame: int, device, stream=None, group=None):
+    """A GvomMap for the ray-segment partition.  With buffer_frames > 1 its
+    workspace lives in torch symmetric memory and the handle gets every rank's
+    workspace pointer (gvom_set_peers): a shifted older map's rows of other
+    slabs are then read from their owners over NVLink.  Returns (map, mapper)."""
+    from .gvom import GvomMap, workspace_bytes
+    P = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    symm = None
+    ws = None
+    if int(grid.get("buffer_frames", 8)) > 1 and P > 1:
+        import torch.distributed._symmetric_memory as symm_mem
+        nbytes = workspace_bytes(grid, max_points_per_frame)
+        ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        symm = symm_mem.rendezvous(ws, grp.group_name)
+    m = GvomMap(grid, max_points_per_frame=max_points_per_frame, device=device, stream=stream,
+                workspace=ws)
+    sm = SegmentMapper(m, group)
+    if symm is not None:
+        m.set_peers(list(symm.buffer_ptrs), sm.ys, rank)
+        sm.symm = symm
+    return m, sm
+
+
 class SegmentMapper:
     """Drives one rank's GvomMap through the ray-segment partition: all
     sensors of the frame are gathered, the rank traces and bins only its rows
     (gvom_integrate_slab), computes the columns of its rows, and the surface
-    rows are all-gathered for phase 1 (slope / roughness / cone search)."""
+    rows are all-gathered for phase 1 (slope / roughness / cone search).  With
+    peers (segment_map, K > 1) device barriers order the owners' integrate
+    before the readers' column pass and the readers before the next integrate."""
 
     def __init__(self, m, group=None):
         self.m = m
@@ -229,12 +286,30 @@ class SegmentMapper:
         self.rank = dist.get_rank(group)
         self.ys = slab_rows(m.ny, self.P)
         self.y0, self.y1 = self.ys[self.rank], self.ys[self.rank + 1]
+        self.symm = None
 
-    def integrate(self, scans_local, gathered: bool = False):
-        """scans_local: this rank's sensors (gathered=True: already all of them)."""
-        scans = scans_local if gathered else all_gather_scans(scans_local, self.group)
+    def _barrier(self):
+        cur = torch.cuda.current_stream(self.m.device)
+        cur.wait_stream(self.m.stream)
+        self.symm.barrier()
+        self.m.stream.wait_stream(cur)
+
+    def integrate(self, scans_local, gathered: bool = False, meta=None):
+        """scans_local: this rank's sensors (gathered=True: already all of them).
+        meta: [(rank, n, pose, rings)] of every sensor in rank order when known
+        on every rank (then only the points move, no host sync)."""
+        if gathered:
+            scans = scans_local
+        elif meta is not None:
+            scans = all_gather_points(scans_local, meta, self.group)
+        else:
+            scans = all_gather_scans(scans_local, self.group)
         torch.cuda.current_stream(self.m.device).wait_stream(torch.cuda.current_stream())
+        if self.symm is not None:  # no peer still reads the slot this frame overwrites
+            self._barrier()
         self.m.integrate_slab(scans, self.y0, self.y1)
+        if self.symm is not None:  # this frame's slabs complete before peers read them
+            self._barrier()
 
     def compute_maps(self):
         self.m.compute_maps_slab(self.y0, self.y1, 0)

@@ -55,6 +55,31 @@ def main():
         if rank == 0:
             print(f"MULTI-GPU {mode} P={P} ok", flush=True)
         del sm, m
+    # ray segments with motion: K = 8 buffered maps in symmetric memory, the
+    # shifted rows of other slabs read from their owners over NVLink
+    w3 = synth.config3(speed=12.0, n_frames=6, columns=512)
+    g3 = dict(w3.grid)
+    npts = w3.points_per_frame
+    ref = GvomMap(g3, max_points_per_frame=npts, device=dev)
+    m, sm = parallel.segment_map(g3, npts, dev)
+    for f in w3.frames:
+        sc = [(torch.from_numpy(s.points).to(dev), s.pose, s.rings) for s in f.scans]
+        ref.shift(f.vehicle_xyz)
+        ref.integrate_scan(sc)
+        m.shift(f.vehicle_xyz)
+        sm.integrate(sc, gathered=True)
+    ref.compute_maps()
+    want = {k: v.cpu().numpy() for k, v in ref.export_layers().items()}
+    sm.compute_maps()
+    lay = m.export_layers()
+    m.synchronize()
+    sl = slice(sm.y0, sm.y1)
+    for k in LAYERS:
+        got = lay[k].cpu().numpy()[sl]
+        assert np.array_equal(np.nan_to_num(got, nan=-7), np.nan_to_num(want[k][sl], nan=-7)), (
+            "segments_motion", k, rank)
+    if rank == 0:
+        print(f"MULTI-GPU segments_motion P={P} ok", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

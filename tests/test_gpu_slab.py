@@ -305,3 +305,54 @@ def test_ray_segment_slabs_c2_and_c3():
 @pytest.mark.slow
 def test_ray_segment_slabs_c5_eight_ranks():
     _run_segments(synth.workload(4), 8)
+
+
+def _run_segments_motion(w, P, K, frames, check_every=3):
+    """Ray segments with motion (K > 1): each rank's buffer maps hold only its
+    slab; a shifted older map's rows of other slabs are read from their
+    owner's workspace (gvom_set_peers: here the P handles' workspaces on one
+    GPU stand in for peer memory).  Compared with one GPU every few frames."""
+    grid = dict(w.grid)
+    grid["buffer_frames"] = K
+    npts = max(f.n_points for f in frames)
+    ref = GvomMap(grid, max_points_per_frame=npts)
+    ms = [GvomMap(grid, max_points_per_frame=npts) for _ in range(P)]
+    ny = ref.ny
+    ys = parallel.slab_rows(ny, P)
+    ptrs = [m.workspace.data_ptr() for m in ms]
+    for r, m in enumerate(ms):
+        m.set_peers(ptrs, ys, r)
+    for i, f in enumerate(frames):
+        scans = [(torch.from_numpy(s.points).cuda(), s.pose, s.rings) for s in f.scans]
+        ref.shift(f.vehicle_xyz)
+        ref.integrate_scan(scans)
+        for r, m in enumerate(ms):
+            m.shift(f.vehicle_xyz)
+            m.integrate_slab(scans, ys[r], ys[r + 1])
+        if (i + 1) % check_every and i != len(frames) - 1:
+            continue
+        ref.compute_maps()
+        ref_layers = layers_np(ref)
+        for r, m in enumerate(ms):
+            m.compute_maps_slab(ys[r], ys[r + 1], 0)
+        surf = torch.cat([ms[r].surface()[ys[r]:ys[r + 1]] for r in range(P)])
+        for r, m in enumerate(ms):
+            m.surface().copy_(surf)
+            m.compute_maps_slab(ys[r], ys[r + 1], 1)
+        torch.cuda.synchronize()
+        for r, m in enumerate(ms):
+            lay = layers_np(m)
+            sl = slice(ys[r], ys[r + 1])
+            for k_ in ("height", "density", "hard", "soft", "spread", "slope", "roughness",
+                       "neg"):
+                a, b = lay[k_][sl], ref_layers[k_][sl]
+                assert np.array_equal(np.nan_to_num(a, nan=-7), np.nan_to_num(b, nan=-7)), \
+                    (i, r, k_)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_ray_segments_with_motion_k8(P):
+    # BASELINE configs[2] (c3, OS1-128, 12 m/s): 8 buffered maps, slabbed, the
+    # shifted rows read over "peer" memory
+    w = synth.config3(speed=12.0, n_frames=12, columns=512)
+    _run_segments_motion(w, P, 8, w.frames)

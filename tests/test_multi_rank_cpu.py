@@ -187,6 +187,12 @@ def _worker_segments(rank, world, port, q):
         assert len(got) == len(scans)
         for (p, pose, rings), (pr, poser) in zip(got, scans):
             assert np.array_equal(p.numpy(), pr) and np.array_equal(pose, poser) and rings == 16
+        # with every sensor's (rank, n, pose, rings) known on every rank, only
+        # the points move
+        meta = [(r, scans[r][0].shape[0], scans[r][1], 16) for r in range(world)]
+        got2 = parallel.all_gather_points(mine, meta)
+        for (p, pose, rings), (pr, poser) in zip(got2, scans):
+            assert np.array_equal(p.numpy(), pr) and np.array_equal(pose, poser) and rings == 16
         dims = (grid["nx"], grid["ny"], grid["nz"])
         nx, ny, nz = dims
         res = grid["res"]

@@ -9,7 +9,7 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'smsp__thread_inst_executed_per_inst_executed.ratio', 'launch__registers_per_thread',
         'lts__throughput.avg.pct_of_peak_sustained_elapsed', 'smsp__inst_executed.sum',
         'smsp__inst_executed_op_global_red.sum', 'dram__throughput.avg.pct_of_peak_sustained_elapsed',
-        'launch__grid_size', 'launch__block_size']
+        'launch__grid_size', 'launch__block_size', 'lts__t_requests_srcunit_tex_op_red.sum']
 STALL = 'smsp__average_warps_issue_stalled_'
 
 
