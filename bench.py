@@ -50,6 +50,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: keep NCCL's banner ("NCCL version ...") off it
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "lidar points/s integrated and map updates/s (256×256×64), % HBM roofline"
 L2_FLUSH_BYTES = 256 << 20
@@ -67,6 +69,8 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent per-GPU frame streams instead of the "
                          "partitioned path")
+    ap.add_argument("--no-l2-probe", action="store_true",
+                    help="skip the L2 reduction-ceiling probe (roofline.l2_red)")
     ap.add_argument("--no-partitioned", action="store_true",
                     help="N = 1: skip the partitioned-path reference line (c5, one rank)")
     ap.add_argument("--frames", type=int, default=4, help="distinct scans cycled")
@@ -681,7 +685,7 @@ def main():
     K = int(w.grid["buffer_frames"])
     maps_ms = stage["maps"][0] / max(stage["maps"][1], 1)
 
-    l2_red = l2_red_ceiling() if rank == 0 else None
+    l2_red = l2_red_ceiling() if rank == 0 and not args.no_l2_probe else None
     red_req = measured_red_requests(w.name)
     if rank == 0:
         cpu = None

@@ -14,7 +14,7 @@ def main(path):
             continue
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
-            if d['Metric Name'] == 'gpu__time_duration.sum':
+            if d['Metric Name'] == 'gpu__time_duration.sum' and 'k_red_probe' not in d['Kernel Name']:
                 nm = d['Kernel Name'].split('(')[0].replace('gvom::<unnamed>::', '')
                 v = float(d['Metric Value'].replace(',', ''))
                 if d['Metric Unit'] == 'usecond':

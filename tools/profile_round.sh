@@ -26,7 +26,7 @@ for mode in segments reduce_scatter fused; do
   echo "slab $mode rc=$?"
 done
 # 4. launch list of the default command (plain run first)
-cmd="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-partitioned"
+cmd="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-partitioned --no-l2-probe"
 timeout 600 $cmd > /dev/null 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_|FillFunctor" --csv \
     --log-file $out/launches.csv $cmd > $out/launches.log 2>&1
