@@ -909,6 +909,8 @@ __device__ __forceinline__ void endpoint_warp(const RayBatch& rb, const Dims& d,
   const int end = __clz(__brev((heads | ~act) & (0xfffffffeu << lane))) - 1;  // run's last lane
   uint32_t cnt = valid ? 1u : 0u, s1 = dz, mn = valid ? dz : 0xffffffffu;
   uint64_t s2 = (uint64_t)dz * dz;
+  // every valid lane its own run (far returns): nothing to reduce
+  if (heads != act)
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t c_o = __shfl_down_sync(0xffffffffu, cnt, o);
@@ -1030,14 +1032,26 @@ __global__ void __launch_bounds__(kTileWords) k_finalize_lut(
   __syncthreads();
   const uint32_t n = stotal;
   const int64_t vbase = b << kTileShift;
-  for (uint32_t i = t; i < n; i += kTileWords) {
-    const int64_t L = vbase + slist[i];
-    const uint32_t rank = off + i;
-    const uint32_t misses = (uint32_t)(-1 - lut[L]);
-    lut[L] = (int32_t)rank;
-    uint4* row = reinterpret_cast<uint4*>(data + rank);
-    row[0] = make_uint4(0u, misses, 0xffffffffu, 0u);
-    row[1] = make_uint4(0u, 0u, 0u, 0u);
+  // eight list entries per thread at a time: all their loads in flight before
+  // any store (a dense tile -- ground near the sensor -- holds thousands)
+  constexpr int kU = 8;
+  for (uint32_t i0 = t; i0 < n; i0 += kU * kTileWords) {
+    int32_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * kTileWords;
+      v[u] = i < n ? __ldcg(lut + vbase + slist[i]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * kTileWords;
+      if (i >= n) break;
+      const uint32_t rank = off + i;
+      lut[vbase + slist[i]] = (int32_t)rank;
+      uint4* row = reinterpret_cast<uint4*>(data + rank);
+      row[0] = make_uint4(0u, (uint32_t)(-1 - v[u]), 0xffffffffu, 0u);
+      row[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
   }
 }
 
