@@ -1158,10 +1158,12 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
   if (cend < 0) cend = (int64_t)d.nx * d.ny;
   if (cend <= cbeg) return cudaSuccess;
   const int64_t lanes = (cend - cbeg) << ss.kp_log2;
-  static int early = -1;  // GVOM_COL_EARLY=0: edge voxels after the band (A/B)
+  // GVOM_COL_EARLY=1: the edge voxels' loads issued before the band's (A/B:
+  // 59 instead of 48 registers, measured slower -- c2 columns 31.1 vs 27.1 us)
+  static int early = -1;
   if (early < 0) {
     const char* e = getenv("GVOM_COL_EARLY");
-    early = e && atoi(e) == 0 ? 0 : 1;
+    early = e && atoi(e) == 1 ? 1 : 0;
   }
   if (early)
     k_columns<true><<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend);
