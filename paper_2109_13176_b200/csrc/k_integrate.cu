@@ -1120,11 +1120,14 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
                                                         *slab);
     return cudaGetLastError();
   }
-  static int split = -1;  // GVOM_RAY_SPLIT=1: two warps per 32 rays (A/B)
-  if (split < 0) {
+  // two warps per 32 rays for frames of more than two waves (c4 -3 %, c5 -4 %;
+  // one- and two-wave frames lose: c2 +7 %); GVOM_RAY_SPLIT=0 / 1 forces it
+  static int split_env = -2;
+  if (split_env == -2) {
     const char* e = getenv("GVOM_RAY_SPLIT");
-    split = e && atoi(e) ? 1 : 0;
+    split_env = e ? (atoi(e) ? 1 : 0) : -1;
   }
+  const bool split = split_env >= 0 ? split_env == 1 : wide;
   if (split && lut_direct) {
     const unsigned b2 = (unsigned)((2 * threads + bs - 1) / bs);
     if (!stream && !wide)

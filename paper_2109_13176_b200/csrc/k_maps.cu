@@ -1205,6 +1205,14 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
   const int rows = lp.row1 - lp.row0;
   int T = (2 * d.nx + 2 * rows + d.sms - 1) / d.sms;
   T = T < 8 ? 8 : ((T + 7) / 8) * 8;
+  {  // GVOM_NEG_T: lines per tile (A/B)
+    static int t_env = -1;
+    if (t_env < 0) {
+      const char* e = getenv("GVOM_NEG_T");
+      t_env = e ? atoi(e) : 0;
+    }
+    if (t_env >= 2) T = t_env;
+  }
   const size_t NB = (size_t)B + 2 * (size_t)K + 2;
   const size_t slot = neg_slot_bytes(B, K), state = neg_state_bytes(B, K);
   // ring depth: as many slots as shared memory allows, up to kNegRing

@@ -1,6 +1,7 @@
-"""The two-warps-per-ray-tile ray cast (k_raycast_split, GVOM_RAY_SPLIT=1: half
-1 resumes every walk at ceil(Tw / 2) from the exact state there) must give the
-oracle's maps bit for bit.  The switch is read once per process, so the parity
+"""The two-warps-per-ray-tile ray cast (k_raycast_split: half 1 resumes every
+walk at ceil(Tw / 2) from the exact state there; the default for frames of
+more than two waves) must give the oracle's maps bit for bit on every frame
+size.  GVOM_RAY_SPLIT=1 forces it and is read once per process, so the parity
 tests run in a child process with it set."""
 import os
 import subprocess
