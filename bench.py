@@ -324,7 +324,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 / r["updates_per_s"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
+        "scaling": "strong" if (world > 1 and not args.replicas) else "weak",
+        "vs_baseline": None, "dtype": "f32+int", "data": "synthetic",
         "config": {"workload": w.name, "points_per_scan": w.points_per_frame,
                    "grid": f"{w.grid['nx']}x{w.grid['ny']}x{w.grid['nz']}@{w.grid['res']}m",
                    "buffer_frames": w.grid["buffer_frames"]},

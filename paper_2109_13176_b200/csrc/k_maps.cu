@@ -100,6 +100,49 @@ __device__ __forceinline__ SlotVox cell_vox(int32_t v, const gvom_voxel* __restr
   return r;
 }
 
+// The column's outputs (lane 0 of its group): q_s and the cone-sweep keys,
+// height, point spread (NEXT-3), band density and hard / soft.
+__device__ __forceinline__ void write_column(const LayerPtrs& out, const LayerParams& lp,
+                                             const Dims& d, int64_t c, int x, int y, int zs,
+                                             int64_t q_s, uint64_t sh, uint64_t s1, uint64_t s2,
+                                             uint64_t SH, uint64_t SW) {
+  out.hard[c] = 0;
+  out.soft[c] = 0;
+  out.nmin[c] = INT32_MAX;
+  out.nmax[c] = INT32_MIN;
+  const int32_t qv = zs < 0 ? kQsUndef : (int32_t)q_s;
+  out.qs[c] = qv;
+  {
+    uint32_t ka, kb;
+    neg_keys(qv, lp, ka, kb);
+    out.negA[c] = ka;
+    out.negB[c] = kb;
+    out.negAT[(int64_t)x * d.ny + y] = ka;
+    out.negBT[(int64_t)x * d.ny + y] = kb;
+  }
+  if (zs < 0) {
+    out.height[c] = __int_as_float(0x7fc00000);
+    out.density[c] = __int_as_float(0x7fc00000);
+    out.spread[c] = __int_as_float(0x7fc00000);
+    return;
+  }
+  {
+    const unsigned __int128 num = (unsigned __int128)sh * s2 - (unsigned __int128)s1 * s1;
+    const double hh = (double)sh, sc = lp.res / 65536.0;
+    out.spread[c] = (float)((double)num / (hh * hh) * (sc * sc));
+  }
+  out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
+  if (SH == 0) {
+    out.density[c] = 0.0f;
+  } else {
+    out.density[c] = (float)((double)SH / (double)SW);
+    if (65536ull * SH >= (uint64_t)lp.tau * SW)
+      out.hard[c] = 1;
+    else
+      out.soft[c] = 1;
+  }
+}
+
 // O7 + O8 fused.  2^lg lanes per output column, lane k <-> buffer map k
 // (32 >> lg columns per warp).  Per column:
 //   z*   : lowest z occupied in any map (OR of the maps' shifted occupancy
@@ -266,46 +309,152 @@ __global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet
   SH = grp_add64(SH, lg);
   SW = grp_add64(SW, lg);
   if (k != 0 || !cvalid) return;
-  out.hard[c] = 0;
-  out.soft[c] = 0;
-  out.nmin[c] = INT32_MAX;
-  out.nmax[c] = INT32_MIN;
-  const int32_t qv = zs < 0 ? kQsUndef : (int32_t)q_s;
-  out.qs[c] = qv;
-  {
-    uint32_t ka, kb;
-    neg_keys(qv, lp, ka, kb);
-    out.negA[c] = ka;
-    out.negB[c] = kb;
-    out.negAT[(int64_t)x * d.ny + y] = ka;
-    out.negBT[(int64_t)x * d.ny + y] = kb;
-  }
-  if (zs < 0) {
-    out.height[c] = __int_as_float(0x7fc00000);
-    out.density[c] = __int_as_float(0x7fc00000);
-    out.spread[c] = __int_as_float(0x7fc00000);
-    return;
-  }
-  {
-    const unsigned __int128 num = (unsigned __int128)sh * s2 - (unsigned __int128)s1 * s1;
-    const double hh = (double)sh, sc = lp.res / 65536.0;
-    out.spread[c] = (float)((double)num / (hh * hh) * (sc * sc));
-  }
-  out.height[c] = (float)(((double)(lp.o_z * 65536 + q_s) * lp.res) / 65536.0);
-  if (SH == 0) {
-    out.density[c] = 0.0f;
-  } else {
-    out.density[c] = (float)((double)SH / (double)SW);
-    if (65536ull * SH >= (uint64_t)lp.tau * SW)
-      out.hard[c] = 1;
-    else
-      out.soft[c] = 1;
-  }
+  write_column(out, lp, d, c, x, y, zs, q_s, sh, s1, s2, SH, SW);
 }
 
 __device__ __forceinline__ int64_t det3(int64_t a, int64_t b, int64_t c, int64_t d, int64_t e,
                                         int64_t f, int64_t g, int64_t h, int64_t i) {
   return a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+}
+
+// O7 + O8 fused, three dependent round trips per column: all occupancy bits
+// of the column at once (nz <= 64) -> the LUT cells of every merged-occupied
+// voxel that can be in the band, z* first (the band lies in [z*, z* + nb],
+// nb = (65535 + T_hi) >> 16, whatever min_dz is) -> their rows, four per batch.
+// Then q_s from z*'s merged min, and each candidate classified: strictly
+// between z_lo and z_hi it is in the band, on z_lo / z_hi its merged min_dz
+// decides (the rule of k_columns, which issues the band and edge loads only
+// after z*'s row: up to eight round trips).  Host: nb < 32 (the 64-z window).
+__global__ void __launch_bounds__(256) k_columns_fast(const __grid_constant__ SlotSet ss,
+                                                      const Dims d, const LayerParams lp,
+                                                      const LayerPtrs out, int64_t cbeg,
+                                                      int64_t cells, int nb) {
+  const int lane = threadIdx.x & 31;
+  const int lg = ss.kp_log2;
+  const int k = lane & ((1 << lg) - 1);
+  const int64_t c0 = cbeg + ((((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << (5 - lg));
+  if (c0 >= cells) return;  // whole warp past the end
+  const int64_t c = c0 + (lane >> lg);
+  const bool cvalid = c < cells;
+  const int x = cvalid ? (int)(c % d.nx) : 0, y = cvalid ? (int)(c / d.nx) : 0;
+  bool col = false;
+  int64_t cb = 0;
+  int dz = 0;
+  const uint32_t* bits = nullptr;
+  const int32_t* lut = nullptr;
+  const gvom_voxel* data = nullptr;
+  if (cvalid && k < ss.K) {
+    const SlotView& s = ss.s[k];
+    const int sx = x + s.dx, sy = y + s.dy;
+    if ((unsigned)sx < (unsigned)d.nx && (unsigned)sy < (unsigned)d.ny) {
+      col = true;
+      cb = (int64_t)d.nz * ((int64_t)sx + (int64_t)d.nx * sy);
+      dz = s.dz;
+      const int64_t dp = peer_delta(ss.pm, sy);  // the row's owner (slab partition)
+      bits = rebase(s.bits, dp);
+      lut = rebase(s.lut, dp);
+      data = rebase(s.data, dp);
+    }
+  }
+  // ---- z*: merged occupancy; a 64-z window from z*'s 32-z chunk ----
+  int zs = -1, zc = 0;
+  uint64_t occ = 0;
+  if (d.nz <= 64) {  // both chunks in flight together
+    uint32_t m0 = col ? col_bits32(bits, d.W, cb, dz, d.nz) : 0u;
+    uint32_t m1 = (col && d.nz > 32) ? col_bits32(bits, d.W, cb, 32 + dz, d.nz) : 0u;
+    m0 = grp_or(m0, lg);
+    m1 = grp_or(m1, lg);
+    occ = ((uint64_t)m1 << 32) | m0;
+    if (occ) zs = __ffsll((long long)occ) - 1;
+  } else {
+    for (int z0 = 0; z0 < d.nz; z0 += 32) {
+      uint32_t m = col ? col_bits32(bits, d.W, cb, z0 + dz, d.nz) : 0u;
+      m = grp_or(m, lg);
+      if (zs >= 0) {
+        if (z0 == zc + 32) occ |= (uint64_t)m << 32;
+      } else if (m) {
+        zs = z0 + __ffs(m) - 1;
+        zc = z0;
+        occ = m;
+      }
+      if (__all_sync(0xffffffffu, zs >= 0 ? z0 >= zc + 32 : !cvalid)) break;
+    }
+  }
+  // ---- candidates: merged-occupied z in [z*, z* + nb] (relative to zc) ----
+  uint64_t cand = 0;
+  if (zs >= 0) {
+    const int r = zs - zc;  // < 32, and nb < 32: the window holds them
+    cand = (occ >> r) & ((2ull << nb) - 1ull);
+    cand <<= r;
+  }
+  uint64_t SH = 0, SW = 0, sh = 0, s1 = 0, s2 = 0;
+  int64_t q_s = 0;
+  int z_lo = 0, z_hi = -1;
+  bool first = true;
+  while (__any_sync(0xffffffffu, cand != 0ull)) {
+    int32_t lv[4];
+    int zz[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      zz[t] = -1;
+      lv[t] = -1;
+      if (cand) {
+        const int z = zc + __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        zz[t] = z;
+        lv[t] = lut_cell(col, lut, cb, z + dz, d.nz);
+      }
+    }
+    SlotVox v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (first && t == 0) {  // z*: the whole row (counts + moments)
+        v[0] = SlotVox{0u, 0u, 0xffffffffu};
+        if (lv[0] >= 0) {
+          const uint4 a = __ldg(reinterpret_cast<const uint4*>(data + lv[0]));
+          const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(data + lv[0]) + 1);
+          v[0] = SlotVox{a.x, a.y, a.z};
+          sh = a.x;
+          s1 = mm.x;
+          s2 = mm.y;
+        } else if (zz[0] >= 0) {
+          v[0].mi = (uint32_t)(-1 - lv[0]);
+        }
+      } else {
+        v[t] = zz[t] >= 0 ? cell_vox(lv[t], data) : SlotVox{0u, 0u, 0xffffffffu};
+      }
+    }
+    if (first) {
+      const uint32_t mn0 = grp_min(v[0].mn, lg);
+      sh = grp_add64(sh, lg);
+      s1 = grp_add64(s1, lg);
+      s2 = grp_add64(s2, lg);
+      q_s = 65536ll * zs + (int64_t)mn0;
+      z_lo = (int)((q_s + lp.T_lo) >> 16);
+      const int64_t zh = (q_s + lp.T_hi) >> 16;
+      z_hi = (int)(zh < (int64_t)d.nz - 1 ? zh : (int64_t)d.nz - 1);
+      first = false;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t mnz = grp_min(v[t].mn, lg);  // the merged min of voxel zz[t]
+      const int z = zz[t];
+      if (z < 0 || zs < 0) continue;
+      bool in = z > z_lo && z < z_hi;
+      if (!in && (z == z_lo || z == z_hi) && mnz != 0xffffffffu) {
+        const int64_t dq = (65536ll * z + (int64_t)mnz) - q_s;
+        in = dq >= lp.T_lo && dq <= lp.T_hi;
+      }
+      if (in) {
+        SH += v[t].h;
+        SW += (uint64_t)v[t].h + v[t].mi;
+      }
+    }
+  }
+  SH = grp_add64(SH, lg);
+  SW = grp_add64(SW, lg);
+  if (k != 0 || !cvalid) return;
+  write_column(out, lp, d, c, x, y, zs, q_s, sh, s1, s2, SH, SW);
 }
 
 // O9: plane fit over the defined in-map cells of the N x N window.
@@ -1158,6 +1307,19 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
   if (cend < 0) cend = (int64_t)d.nx * d.ny;
   if (cend <= cbeg) return cudaSuccess;
   const int64_t lanes = (cend - cbeg) << ss.kp_log2;
+  // the three-round-trip kernel when the band fits the 64-z window
+  // (GVOM_COL_FAST=0: the original kernel, A/B)
+  static int fast = -1;
+  if (fast < 0) {
+    const char* e = getenv("GVOM_COL_FAST");
+    fast = e && atoi(e) == 0 ? 0 : 1;
+  }
+  const int64_t nb = (65535 + lp.T_hi) >> 16;
+  if (fast && nb < 32) {
+    k_columns_fast<<<(unsigned)((lanes + 255) / 256), 256, 0, st>>>(ss, d, lp, out, cbeg, cend,
+                                                                     (int)nb);
+    return cudaGetLastError();
+  }
   // GVOM_COL_EARLY=1: the edge voxels' loads issued before the band's (A/B:
   // 59 instead of 48 registers, measured slower -- c2 columns 31.1 vs 27.1 us)
   static int early = -1;
