@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--neg8cone", action="store_true",
                     help="GVOM_FLAG_NEG_8CONE variant (8-cone negative-obstacle search)")
+    ap.add_argument("--no-balance", action="store_true",
+                    help="ray segments: keep equal-row slabs (default: bounds rebalanced "
+                         "once from the warm-up frame's per-row work, gvom_row_work)")
     ap.add_argument("--slab-mode", default="segments",
                     choices=["segments", "reduce_scatter", "fused"],
                     help="partitioned path: ray segments per slab (default), the dense "
@@ -354,7 +357,8 @@ def ensure_dist(dev):
     dist.init_process_group("nccl", device_id=dev)
 
 
-def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int = 1):
+def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int = 1,
+                 balance: bool = True):
     """the points of ONE frame are sharded across the ranks (sensor
     i -> rank i % N).  mode "segments": the points are all-gathered and each
     rank traces only the ray segments inside its y-slab; "reduce_scatter":
@@ -400,12 +404,16 @@ def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int
             sm.integrate(mine)
         sm.compute_maps()
 
+    balanced = mode == "segments" and balance and world > 1
     with torch.cuda.stream(stream):
-        for _ in range(warmup):
+        for i in range(warmup):
             step()
+            if balanced and i == 0:  # slab bounds from the first frame's row work
+                sm.rebalance()
         torch.cuda.synchronize()
         dist.barrier()
         total = 0.0
+        n0 = m.launch_count()
         with ClockSampler(local) as clk:
             for _ in range(steps):
                 flush.zero_()
@@ -415,6 +423,7 @@ def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int
                 b.record(stream)
                 b.synchronize()
                 total += a.elapsed_time(b)
+        launches = m.launch_count() - n0
         dist.barrier()
     t = torch.tensor([total], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -433,10 +442,13 @@ def slab_measure(cfg_index: int, steps: int, warmup: int, mode: str, frames: int
                                        "segments inside its rows (gvom_integrate_slab)",
                            "fused": "miss grids summed over peer memory in the slab finalize",
                            "reduce_scatter": "reduce-scatter of the miss grids by y-slab"}[mode],
+                       "slabs": list(sm.ys),
+                       "slab_bounds": ("rebalanced from the warm-up frame's per-row work "
+                                       "(gvom_row_work)") if balanced else "equal rows",
                        "l2": "flushed (256 MiB write) between steps",
                        "step": "shift+partial_scan+exchange+slab_finalize+slab maps"},
             "map_updates_per_s": steps / (total / 1e3),
-            "gpu_launches": None, "clocks": clk.summary(),
+            "gpu_launches": launches, "clocks": clk.summary(),
         }
     del sm, m
     dist.barrier()
@@ -448,7 +460,8 @@ def main_slab(args):
     configs[4], the multi-GPU workload; --config chooses another)."""
     import torch.distributed as dist
     cfg = 4 if args.config is None else args.config
-    line = slab_measure(cfg, args.steps, args.warmup, args.slab_mode)
+    line = slab_measure(cfg, args.steps, args.warmup, args.slab_mode,
+                        balance=not args.no_balance)
     if line is not None:
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -219,6 +219,16 @@ GVOM_API gvom_status gvom_integrate_slab(gvom_handle* h, const gvom_scan* scans,
 GVOM_API gvom_status gvom_set_peers(gvom_handle* h, const void* const* d_peer_workspaces,
                                     const int32_t* slab_y, int32_t n_ranks, int32_t rank);
 
+/* Slab balancing for the ray-segment partition: d_out[y] (device, u64 [ny];
+ * only [y0, y1) written) = the pass-throughs + returns of row y in the newest
+ * buffer map, i.e. the sum over the row's voxels of misses + hits (P:105,
+ * the counts the ray cast and the binning added).  A rank's ray-cast
+ * work in its rows is proportional to it, so slab bounds that split the
+ * summed rows evenly (parallel.balanced_slab_rows) even out the ranks.
+ * Stream-ordered after the last integrate; not for rolling maps
+ * (GVOM_E_INVALID); GVOM_E_EMPTY before the first integrate.              */
+GVOM_API gvom_status gvom_row_work(gvom_handle* h, int32_t y0, int32_t y1, uint64_t* d_out);
+
 /* Map processing: combine all buffer maps at the origin of the
  * newest one, then compute height, density, hard, soft, slope,
  * roughness and negative-obstacle layers.  GVOM_E_EMPTY if no map.         */

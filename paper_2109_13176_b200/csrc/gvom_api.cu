@@ -1367,6 +1367,17 @@ gvom_status gvom_set_peers(gvom_handle* h, const void* const* d_peer_workspaces,
   return GVOM_OK;
 }
 
+gvom_status gvom_row_work(gvom_handle* h, int32_t y0, int32_t y1, uint64_t* d_out) {
+  NvtxRange nvtx_("gvom_row_work");
+  if (!h || h->rolling || !d_out || y0 < 0 || y1 > h->cfg.ny || y0 >= y1) return GVOM_E_INVALID;
+  if (h->count == 0) return GVOM_E_EMPTY;
+  const Slot& slot = h->slots[(h->head - 1 + h->NS) % h->NS];
+  GVOM_CU(stage(h, GVOM_STAGE_EXPORT, true, [&] {
+    return launch_row_work(slot.lut, slot.data, h->d, y0, y1, (unsigned long long*)d_out, h->st);
+  }));
+  return GVOM_OK;
+}
+
 gvom_status gvom_slab_complete(gvom_handle* h, int64_t k_total) {
   NvtxRange nvtx_("gvom_slab_complete");
   if (!h || h->pipelined || h->rolling || h->count == 0 || k_total < 0 || k_total > h->lay.cap)

@@ -250,6 +250,9 @@ cudaError_t launch_roll_export(const RollGrid& g, const Dims& d, uint64_t* hits,
                                uint32_t* min_dz, uint64_t* m1, uint64_t* m2, cudaStream_t st);
 
 // ---- multi-GPU slab partition (k_slab.cu) ----
+// out[y] for y in [y0, y1): pass-throughs + returns of row y (slab balancing)
+cudaError_t launch_row_work(const int32_t* lut, const gvom_voxel* data, const Dims& d, int32_t y0,
+                            int32_t y1, unsigned long long* out, cudaStream_t st);
 struct SlabBounds {
   int32_t P;
   int32_t y[GVOM_MAX_RANKS + 1];  // slab r = rows [y[r], y[r+1])

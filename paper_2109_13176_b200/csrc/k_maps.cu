@@ -1307,12 +1307,13 @@ cudaError_t launch_columns(const SlotSet& ss, const Dims& d, const LayerParams& 
   if (cend < 0) cend = (int64_t)d.nx * d.ny;
   if (cend <= cbeg) return cudaSuccess;
   const int64_t lanes = (cend - cbeg) << ss.kp_log2;
-  // the three-round-trip kernel when the band fits the 64-z window
-  // (GVOM_COL_FAST=0: the original kernel, A/B)
+  // GVOM_COL_FAST=1: the three-round-trip kernel when the band fits the 64-z
+  // window (A/B; 62 registers, measured slower on c2/c3 -- columns 33.2 vs
+  // 27.1 us -- and a tie on c4, so off by default)
   static int fast = -1;
   if (fast < 0) {
     const char* e = getenv("GVOM_COL_FAST");
-    fast = e && atoi(e) == 0 ? 0 : 1;
+    fast = e && atoi(e) == 1 ? 1 : 0;
   }
   const int64_t nb = (65535 + lp.T_hi) >> 16;
   if (fast && nb < 32) {

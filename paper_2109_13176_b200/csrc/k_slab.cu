@@ -174,6 +174,50 @@ __global__ void __launch_bounds__(256) k_bits_from_lut(const int32_t* __restrict
 
 inline unsigned blocks_for(int64_t n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
 
+
+// Per-row work of a frame map (slab balancing): row y's pass-throughs + returns
+// = sum over its voxels of misses + hits -- for an empty voxel the O6 code
+// -1 - N_m, for an occupied one its data row.  One block per row, int4 LUT
+// loads, the data rows only behind occupied entries.
+__global__ void __launch_bounds__(256) k_row_work(const int32_t* __restrict__ lut,
+                                                  const gvom_voxel* __restrict__ data,
+                                                  const Dims d, int32_t y0,
+                                                  unsigned long long* __restrict__ out) {
+  const int64_t row = (int64_t)d.nx * d.nz;
+  const int64_t y = (int64_t)y0 + blockIdx.x;
+  const int32_t* lr = lut + y * row;
+  unsigned long long acc = 0ull;
+  auto add = [&](int32_t e) {
+    if (e < 0) {
+      acc += (unsigned)(-1 - e);
+    } else {
+      const gvom_voxel& v = data[e];
+      acc += (unsigned long long)__ldg(&v.misses) + __ldg(&v.hits);
+    }
+  };
+  if ((row & 3) == 0) {  // rows start 16-byte aligned
+    const int4* l4 = reinterpret_cast<const int4*>(lr);
+    for (int64_t i = threadIdx.x; i < (row >> 2); i += blockDim.x) {
+      const int4 q = __ldcs(l4 + i);
+      add(q.x);
+      add(q.y);
+      add(q.z);
+      add(q.w);
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < row; i += blockDim.x) add(__ldcs(lr + i));
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ unsigned long long ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0ull;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    out[y] = t;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_ep_count(const float4* pts, int64_t n, const SensorParams& sp, const Dims& d,
@@ -220,6 +264,13 @@ cudaError_t launch_bits_from_lut(const int32_t* lut, uint32_t* bits, uint32_t* w
 cudaError_t launch_transpose_init(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                                   cudaStream_t st) {
   k_transpose_init<<<blocks_for((int64_t)d.nx * d.ny, 256), 256, 0, st>>>(d, lp, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_work(const int32_t* lut, const gvom_voxel* data, const Dims& d, int32_t y0,
+                            int32_t y1, unsigned long long* out, cudaStream_t st) {
+  if (y1 <= y0) return cudaSuccess;
+  k_row_work<<<(unsigned)(y1 - y0), 256, 0, st>>>(lut, data, d, y0, out);
   return cudaGetLastError();
 }
 

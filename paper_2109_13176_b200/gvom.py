@@ -90,6 +90,7 @@ def load_library() -> C.CDLL:
         "gvom_integrate_scan": ([P, P, I32], I32),
         "gvom_integrate_slab": ([P, P, I32, I32, I32], I32),
         "gvom_set_peers": ([P, P, P, I32, I32], I32),
+        "gvom_row_work": ([P, I32, I32, P], I32),
         "gvom_compute_maps": ([P], I32),
         "gvom_export_2d": ([P, I32, P, C.c_size_t], I32),
         "gvom_export_layers": ([P, P, P], I32),
@@ -135,7 +136,7 @@ EXPORTED = ("gvom_workspace_bytes", "gvom_create", "gvom_destroy", "gvom_set_str
             "gvom_step", "gvom_graph_stats", "gvom_export_layers_cost", "gvom_export_window",
             "gvom_slot_buffers", "gvom_slab_complete", "gvom_slab_finalize_peers",
             "gvom_obstacle_buffers", "gvom_debug_inject_fault", "gvom_integrate_slab",
-            "gvom_set_peers")
+            "gvom_set_peers", "gvom_row_work")
 
 
 def make_config(grid: dict, max_points_per_frame: int) -> Config:
@@ -382,6 +383,20 @@ class GvomMap:
         ys = (C.c_int32 * (P + 1))(*[int(v) for v in slab_y]) if P else None
         _check(self.lib.gvom_set_peers(self.h, ws if P else None, ys, P, int(rank)),
                "gvom_set_peers")
+
+    def row_work(self, y0: int = 0, y1: Optional[int] = None,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """gvom_row_work: int64 [ny] on the device, rows [y0, y1) = the
+        pass-throughs + returns of each row of the newest buffer map (the
+        others untouched; zeros when `out` is None)."""
+        y1 = self.ny if y1 is None else y1
+        if out is None:
+            out = torch.zeros(self.ny, dtype=torch.int64, device=self.device)
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        assert out.dtype == torch.int64 and out.is_cuda and out.numel() == self.ny
+        _check(self.lib.gvom_row_work(self.h, int(y0), int(y1), C.c_void_p(out.data_ptr())),
+               "gvom_row_work")
+        return out
 
     def compute_maps(self):
         _check(self.lib.gvom_compute_maps(self.h), "gvom_compute_maps")

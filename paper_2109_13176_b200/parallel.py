@@ -6,7 +6,11 @@ Two partitions of the same frame, both exact (identical to one GPU):
   every sensor's points (all_gather_scans: 16 bytes per point) and
   gvom_integrate_slab traces only the part of each ray inside its own rows --
   no dense count grid leaves a GPU, nothing is reduced; the surface rows are
-  all-gathered for the plane fits and the cone search.
+  all-gathered for the plane fits and the cone search.  A rank's work is the
+  steps inside its rows, which crowd around the vehicle, so the slab bounds
+  can be rebalanced from a frame's per-row work (SegmentMapper.rebalance:
+  gvom_row_work, all_reduce, balanced_slab_rows); uneven slabs gather
+  through one padded all-gather.
 * reduce-scatter (SlabMapper, the north_star's design): every rank traces its
   own sensors' rays whole into a dense partial miss grid, and the grids are
   combined by slab as below.
@@ -46,6 +50,33 @@ def slab_rows(ny: int, P: int) -> List[int]:
     if ny % P:
         raise ValueError(f"ny={ny} is not divisible by {P} ranks")
     return [r * (ny // P) for r in range(P + 1)]
+
+
+def balanced_slab_rows(row_work: Sequence[float], P: int, row_share: float = 0.1) -> List[int]:
+    """Slab bounds [y_0 = 0, ..., y_P = ny] that split the rows' work evenly
+    (ray-segment partition, gvom_row_work: a rank traces only the steps in its
+    rows).  Row weight = its pass-throughs + returns + a per-row constant
+    carrying `row_share` of the total (the column / plane-fit / cone passes,
+    which cost the same on every row); bound k is the row where the running
+    weight is nearest k/P of the total, every slab at least one row.  Pure
+    host arithmetic on the same all-reduced vector, so every rank agrees."""
+    import numpy as np
+    w = np.asarray(row_work, dtype=np.float64)
+    ny = int(w.shape[0])
+    if P < 1 or P > ny:
+        raise ValueError(f"{P} slabs over {ny} rows")
+    tot = float(w.sum())
+    w = w + (row_share * tot / ny if tot > 0 else 1.0)
+    cum = np.concatenate([[0.0], np.cumsum(w)])  # cum[y] = weight of rows [0, y)
+    ys = [0]
+    for k in range(1, P):
+        t = cum[-1] * k / P
+        y = int(np.searchsorted(cum, t))  # cum[y - 1] < t <= cum[y]
+        if y > 0 and t - cum[y - 1] < cum[y] - t:
+            y -= 1
+        ys.append(min(max(y, ys[-1] + 1), ny - (P - k)))
+    ys.append(ny)
+    return ys
 
 
 def exchange_misses(miss_full: torch.Tensor, group=None) -> torch.Tensor:
@@ -97,10 +128,25 @@ def gather_frame(lut: torch.Tensor, data: torch.Tensor, rows: int, y0: int, y1: 
             dist.broadcast(data[bases[r]:bases[r] + ks[r]], src=r, group=group)
 
 
-def gather_rows(full: torch.Tensor, y0: int, y1: int, group=None):
-    """all-gather equal row slabs of a [ny, ...] tensor in place."""
-    mine = full[y0:y1].contiguous().clone()
-    dist.all_gather_into_tensor(full.view(-1), mine.view(-1), group=group)
+def gather_rows(full: torch.Tensor, y0: int, y1: int, group=None,
+                ys: Optional[Sequence[int]] = None):
+    """all-gather the row slabs of a [ny, ...] tensor in place (equal slabs,
+    or the bounds `ys`: uneven slabs go through one padded all-gather)."""
+    P = dist.get_world_size(group)
+    rows = [ys[r + 1] - ys[r] for r in range(P)] if ys is not None else None
+    if rows is None or len(set(rows)) == 1:
+        mine = full[y0:y1].contiguous().clone()
+        dist.all_gather_into_tensor(full.view(-1), mine.view(-1), group=group)
+        return
+    cap = max(rows)
+    per = full[0].numel()
+    mine = torch.zeros((cap, per), dtype=full.dtype, device=full.device)
+    mine[:y1 - y0] = full[y0:y1].reshape(y1 - y0, per)
+    allr = torch.empty((P * cap, per), dtype=full.dtype, device=full.device)
+    dist.all_gather_into_tensor(allr, mine, group=group)
+    fv = full.view(full.shape[0], per)
+    for r in range(P):
+        fv[ys[r]:ys[r + 1]] = allr[r * cap:r * cap + rows[r]]
 
 
 class SlabMapper:
@@ -246,7 +292,8 @@ def global_rank_base(k_local: torch.Tensor, group=None):
     return allk[:r].sum(), allk.sum()
 
 
-def segment_map(grid: dict, max_points_per_frame: int, device, stream=None, group=None):
+def segment_map(grid: dict, max_points_per_frame: int, device, stream=None, group=None,
+                ys: Optional[Sequence[int]] = None):
     """A GvomMap for the ray-segment partition.  With buffer_frames > 1 its
     workspace lives in torch symmetric memory and the handle gets every rank's
     workspace pointer (gvom_set_peers): a shifted older map's rows of other
@@ -264,7 +311,7 @@ def segment_map(grid: dict, max_points_per_frame: int, device, stream=None, grou
         symm = symm_mem.rendezvous(ws, grp.group_name)
     m = GvomMap(grid, max_points_per_frame=max_points_per_frame, device=device, stream=stream,
                 workspace=ws)
-    sm = SegmentMapper(m, group)
+    sm = SegmentMapper(m, group, ys)
     if symm is not None:
         m.set_peers(list(symm.buffer_ptrs), sm.ys, rank)
         sm.symm = symm
@@ -279,14 +326,36 @@ class SegmentMapper:
     peers (segment_map, K > 1) device barriers order the owners' integrate
     before the readers' column pass and the readers before the next integrate."""
 
-    def __init__(self, m, group=None):
+    def __init__(self, m, group=None, ys: Optional[Sequence[int]] = None):
         self.m = m
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.ys = slab_rows(m.ny, self.P)
-        self.y0, self.y1 = self.ys[self.rank], self.ys[self.rank + 1]
         self.symm = None
+        self._set_bounds(list(ys) if ys is not None else slab_rows(m.ny, self.P))
+
+    def _set_bounds(self, ys):
+        if (len(ys) != self.P + 1 or ys[0] != 0 or ys[-1] != self.m.ny or
+                any(b <= a for a, b in zip(ys, ys[1:]))):
+            raise ValueError(f"bad slab bounds {ys}")
+        self.ys = ys
+        self.y0, self.y1 = ys[self.rank], ys[self.rank + 1]
+
+    def rebalance(self, row_share: float = 0.1) -> List[int]:
+        """New slab bounds from the last frame's per-row work (gvom_row_work
+        of this rank's rows, all-reduced; balanced_slab_rows); the next
+        integrate uses them.  One host synchronisation -- call it between
+        frames, not every frame.  Not with peers (buffer_frames > 1): the
+        older buffer maps' rows stay with the owners that integrated them."""
+        if self.symm is not None:
+            raise RuntimeError("slab bounds are fixed once peers are set")
+        work = self.m.row_work(self.y0, self.y1)
+        cur = torch.cuda.current_stream(self.m.device) if work.is_cuda else None
+        if cur is not None:
+            cur.wait_stream(self.m.stream)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM, group=self.group)
+        self._set_bounds(balanced_slab_rows(work.cpu().numpy(), self.P, row_share))
+        return self.ys
 
     def _barrier(self):
         cur = torch.cuda.current_stream(self.m.device)
@@ -315,9 +384,9 @@ class SegmentMapper:
         self.m.compute_maps_slab(self.y0, self.y1, 0)
         cur = torch.cuda.current_stream(self.m.device)
         cur.wait_stream(self.m.stream)
-        gather_rows(self.m.surface(), self.y0, self.y1, self.group)
+        gather_rows(self.m.surface(), self.y0, self.y1, self.group, self.ys)
         if int(self.m.cfg.flags) & 2:  # GVOM_FLAG_SLOPE_SKIP_OBSTACLES: windows read them
             for t in self.m.obstacles():
-                gather_rows(t, self.y0, self.y1, self.group)
+                gather_rows(t, self.y0, self.y1, self.group, self.ys)
         self.m.stream.wait_stream(cur)
         self.m.compute_maps_slab(self.y0, self.y1, 1)

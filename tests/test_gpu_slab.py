@@ -231,7 +231,7 @@ def _moved(pose, dx):
     return p
 
 
-def _run_segments(w, P):
+def _run_segments(w, P, ys=None):
     """The ray-segment slab partition (gvom_integrate_slab): every rank sees
     every sensor and traces only the part of each ray inside its rows; its
     buffer map holds the slab with LOCAL ranks (global = the k of the slabs
@@ -248,7 +248,7 @@ def _run_segments(w, P):
     ref_lut, ref_data, _ = ref.export_frame(0)
     ref_layers = layers_np(ref)
     nx, ny, nz = ref.nx, ref.ny, ref.nz
-    ys = parallel.slab_rows(ny, P)
+    ys = parallel.slab_rows(ny, P) if ys is None else ys
     row = nx * nz
     ranks = []
     for r in range(P):
@@ -300,6 +300,58 @@ def test_ray_segment_slabs_c1(P):
 def test_ray_segment_slabs_c2_and_c3():
     _run_segments(synth.workload(1), 4)
     _run_segments(synth.config3(speed=12.0, n_frames=1), 8)
+
+
+def _oracle_row_work(w):
+    """Per-row pass-throughs + returns of frame 0 from the oracle's dense
+    counts (integrate_dense: H and M per voxel)."""
+    from oracle import oracle as O
+    om = O.OracleMap(w.grid)
+    f = w.frames[0]
+    om.shift(f.vehicle_xyz)
+    H, M, _, _, _, _ = O.integrate_dense(om.dims, [(s.points, s.pose) for s in f.scans],
+                                         om.res, om.origin)
+    nx, ny, nz = om.dims
+    return (H.astype(np.int64) + M).reshape(ny, nx * nz).sum(axis=1)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_row_work_matches_oracle(cfg):
+    # gvom_row_work (slab balancing) = sum over each row's voxels of the
+    # oracle's hits + misses; on a slab handle only its rows are written
+    w = synth.workload(cfg)
+    want = _oracle_row_work(w)
+    grid = dict(w.grid)
+    grid["buffer_frames"] = 1
+    f = w.frames[0]
+    scans = [(torch.from_numpy(s.points).cuda(), s.pose, s.rings) for s in f.scans]
+    m = GvomMap(grid, max_points_per_frame=f.n_points)
+    m.shift(f.vehicle_xyz)
+    m.integrate_scan(scans)
+    got = m.row_work()
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), want)
+    ny = m.ny
+    y0, y1 = ny // 3, ny // 3 + 5
+    s = GvomMap(grid, max_points_per_frame=f.n_points)
+    s.shift(f.vehicle_xyz)
+    s.integrate_slab(scans, y0, y1)
+    out = torch.full((ny,), -7, dtype=torch.int64, device="cuda")
+    s.row_work(y0, y1, out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.array_equal(o[y0:y1], want[y0:y1]) and (np.delete(o, np.s_[y0:y1]) == -7).all()
+
+
+@pytest.mark.parametrize("cfg,P", [(3, 4), (1, 8), (0, 5)])
+def test_ray_segment_slabs_balanced(cfg, P):
+    # uneven slab bounds from the measured row work (SegmentMapper.rebalance):
+    # the partition stays exact whatever the bounds (c1 at P = 5: slabs that
+    # do not divide the rows, several sharing finalize tiles)
+    w = synth.workload(cfg)
+    ys = parallel.balanced_slab_rows(_oracle_row_work(w), P)
+    assert ys != parallel.slab_rows(w.grid["ny"], P) if w.grid["ny"] % P == 0 else True
+    _run_segments(w, P, ys)
 
 
 @pytest.mark.slow

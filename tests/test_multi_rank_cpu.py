@@ -167,6 +167,39 @@ def test_slab_rows():
         parallel.slab_rows(100, 8)
 
 
+def test_balanced_slab_rows():
+    from paper_2109_13176_b200 import parallel
+    # uniform work: equal slabs
+    assert parallel.balanced_slab_rows([5] * 64, 4) == [0, 16, 32, 48, 64]
+    # all work in the middle rows: the middle slabs get narrow
+    w = np.zeros(64)
+    w[24:40] = 100.0
+    ys = parallel.balanced_slab_rows(w, 4, row_share=0.0)
+    assert ys[0] == 0 and ys[-1] == 64 and 24 <= ys[1] < ys[2] < ys[3] <= 40
+    # property on random work: monotone, >= 1 row each, every bound within
+    # half a row weight of its target (unless clamped), all ranks agree
+    rng = np.random.default_rng(3)
+    for trial in range(50):
+        ny = int(rng.integers(8, 300))
+        P = int(rng.integers(1, min(ny, 16) + 1))
+        w = rng.gamma(0.5, 100.0, ny) * (rng.random(ny) < 0.8)
+        ys = parallel.balanced_slab_rows(w, P, row_share=0.1)
+        assert len(ys) == P + 1 and ys[0] == 0 and ys[-1] == ny
+        assert all(b > a for a, b in zip(ys, ys[1:]))
+        ww = w + 0.1 * w.sum() / ny if w.sum() > 0 else w + 1.0
+        cum = np.concatenate([[0.0], np.cumsum(ww)])
+        for k in range(1, P):
+            t = cum[-1] * k / P
+            y = ys[k]
+            clamped = y == ys[k - 1] + 1 or y == ny - (P - k)
+            assert clamped or (abs(cum[y] - t) <= ww[y - 1] / 2 + 1e-9 * cum[-1] or
+                               abs(cum[y] - t) <= ww[min(y, ny - 1)] / 2 + 1e-9 * cum[-1]), \
+                (trial, k, y)
+        assert parallel.balanced_slab_rows(w, P, row_share=0.1) == ys
+    with pytest.raises(ValueError):
+        parallel.balanced_slab_rows([1.0] * 4, 5)
+
+
 def _worker_segments(rank, world, port, q):
     """The ray-segment partition's exchange: all_gather_scans must hand every
     rank every sensor (bit-identical points, poses, ring counts, rank order),
@@ -207,6 +240,32 @@ def _worker_segments(rank, world, port, q):
         occ = ref.lut[v0:v1] >= 0
         if occ.any():  # the slab's first occupied voxel has global rank = base
             assert int(ref.lut[v0:v1][occ][0]) == int(base)
+        # balanced slabs (SegmentMapper.rebalance's arithmetic): each rank's
+        # rows of the oracle's per-row pass-throughs + returns, all-reduced,
+        # give the same uneven bounds on both ranks; the surface rows then
+        # travel through the padded all-gather and the global ranks still
+        # line up with the single-process frame
+        work = (H + M).reshape(ny, nx * nz).sum(axis=1).astype(np.int64)
+        mine_w = np.zeros(ny, np.int64)
+        mine_w[ys[rank]:ys[rank + 1]] = work[ys[rank]:ys[rank + 1]]
+        wt = torch.from_numpy(mine_w)
+        dist.all_reduce(wt)
+        assert np.array_equal(wt.numpy(), work)
+        yb = parallel.balanced_slab_rows(wt.numpy(), world)
+        allyb = [None] * world
+        dist.all_gather_object(allyb, yb)
+        assert all(a == yb for a in allyb) and yb != ys, (yb, ys)
+        full = torch.full((ny, 3), -1.0)
+        full[yb[rank]:yb[rank + 1]] = torch.arange(yb[rank], yb[rank + 1]).float()[:, None]
+        parallel.gather_rows(full, yb[rank], yb[rank + 1], None, yb)
+        assert torch.equal(full, torch.arange(ny).float()[:, None].expand(ny, 3))
+        v0, v1 = yb[rank] * nx * nz, yb[rank + 1] * nx * nz
+        k_b = int((H[v0:v1] >= 1).sum())
+        base_b, total_b = parallel.global_rank_base(torch.tensor(k_b, dtype=torch.int64))
+        assert int(total_b) == ref.k
+        occ = ref.lut[v0:v1] >= 0
+        if occ.any():
+            assert int(ref.lut[v0:v1][occ][0]) == int(base_b)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok", k_local, int(base)))
