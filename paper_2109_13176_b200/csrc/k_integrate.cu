@@ -434,7 +434,11 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
         newtile = (atomicOr(bits + (LE >> 5), bit) & bit) ? 0xffffffffu : (LE >> kTileShift);
       }
       const int R = rem[0] + rem[1] + rem[2];
-      if (R > 0) {
+      // kSlab: a segment whose rows [min(S_y, E_y), max(S_y, E_y)] miss the slab
+      // has no step there -- skip its setup (most rays of an outer slab)
+      const bool miss_slab =
+          kSlab && (max(sp.S[1], E[1]) < sr.y0 || min(sp.S[1], E[1]) >= sr.y1);
+      if (R > 0 && !miss_slab) {
         bool ok = fin;
         float Kend = 0.f;
         int Aend = -1;

@@ -52,7 +52,7 @@ def slab_rows(ny: int, P: int) -> List[int]:
     return [r * (ny // P) for r in range(P + 1)]
 
 
-def balanced_slab_rows(row_work: Sequence[float], P: int, row_share: float = 0.1) -> List[int]:
+def balanced_slab_rows(row_work: Sequence[float], P: int, row_share: float = 0.25) -> List[int]:
     """Slab bounds [y_0 = 0, ..., y_P = ny] that split the rows' work evenly
     (ray-segment partition, gvom_row_work: a rank traces only the steps in its
     rows).  Row weight = its pass-throughs + returns + a per-row constant
@@ -341,7 +341,7 @@ class SegmentMapper:
         self.ys = ys
         self.y0, self.y1 = ys[self.rank], ys[self.rank + 1]
 
-    def rebalance(self, row_share: float = 0.1) -> List[int]:
+    def rebalance(self, row_share: float = 0.25) -> List[int]:
         """New slab bounds from the last frame's per-row work (gvom_row_work
         of this rank's rows, all-reduced; balanced_slab_rows); the next
         integrate uses them.  One host synchronisation -- call it between
