@@ -14,7 +14,9 @@ value  = lidar points integrated per second over whole steps (all ranks),
          inputs resident in HBM, L2 flushed (256 MiB write) between steps,
          device time from CUDA events on the library's stream.
 e2e    = same metric through the public API with pinned HOST buffers: H2D of
-         the scan and D2H of all 7 layers inside every timed step.
+         every scan and D2H of all layers of every step inside the timed region
+         (value: the pipelined handle streaming scans back to back; the
+         synchronous step-at-a-time numbers beside it).
 roofline = the dominant kernel (ray cast): algorithmic bytes per launch
          (16 N + 8 M + 8 H) / its mean event-timed launch
          duration, against MEASURED_PEAKS.json hbm_gbs.
@@ -500,6 +502,32 @@ def pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier):
     return ms
 
 
+def e2e_line(npts, steps, world, sync_value, sync_wall_s, pipe_s, d2h_bytes):
+    """The e2e object: a user's stream of scans through gvom_step with pinned
+    host buffers -- H2D of every scan and D2H of every step's 8 layers inside
+    the timed region.  value = the pipelined handle (GVOM_FLAG_PIPELINE: scan
+    t+1's copy and integrate overlap map processing t), wall clock over
+    the whole sequence; the synchronous numbers (one step at a time) beside it.
+    The rolling map cannot pipeline: value = the synchronous one there."""
+    sync_wall = npts * steps * world / sync_wall_s
+    piped = None if math.isnan(pipe_s) else npts * steps * world / pipe_s
+    return {
+        "value": piped if piped is not None else sync_value, "unit": "points/s",
+        "mode": "pipelined" if piped is not None else "synchronous",
+        "h2d_bytes_per_step": 16 * npts, "d2h_bytes_per_step": d2h_bytes, "steps": steps,
+        "timing": ("GVOM_FLAG_PIPELINE handle through gvom_step, pinned host points in, all "
+                   "layers out to pinned host (outputs double-buffered), steps submitted back to "
+                   "back, wall clock over the sequence to the final synchronize")
+        if piped is not None else "CUDA events around each synchronous gvom_step",
+        "synchronous_value": sync_value,
+        "synchronous_timing": "CUDA events around each gvom_step (pinned host points in, 8 "
+                              "layers out to pinned host), synchronised every step",
+        "synchronous_wall_value": sync_wall,
+        "synchronous_wall_timing": "perf_counter around the host call + synchronize (host "
+                                   "submit and ctypes marshalling included; L2 flush outside)",
+    }
+
+
 def pipelined_e2e_s(w, frames, host_frames, host_outs, npts, dev, stream, steps, args, barrier):
     """End to end with the pipelined handle: pinned host points in, all layers
     out to pinned host (two output sets, alternating), steps submitted back to
@@ -751,19 +779,8 @@ def main():
             "stages_ms_per_step": {s: v[0] / n_inst for s, v in stage_all.items() if v[1]},
             "stages_note": "separate instrumented pass (events around every launch, "
                            "separate calls without a graph)",
-            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * npts,
-                    "d2h_bytes_per_step": m.nx * m.ny * (4 * 5 + 3), "steps": e2e_steps,
-                    "timing": "CUDA events around each gvom_step (pinned host points in, 8 "
-                              "layers out to pinned host), synchronised every step",
-                    "wall_value": npts * e2e_steps * world / e2e_wall,
-                    "wall_timing": "perf_counter around the host call + synchronize (host "
-                                   "submit and ctypes marshalling included; L2 flush outside)",
-                    "pipelined_value": (None if math.isnan(pipe_e2e_s)
-                                        else npts * e2e_steps * world / pipe_e2e_s),
-                    "pipelined_timing": "GVOM_FLAG_PIPELINE handle, same host buffers in and "
-                                        "out (outputs double-buffered), steps submitted back "
-                                        "to back, wall clock over the sequence to the final "
-                                        "synchronize"},
+            "e2e": e2e_line(npts, e2e_steps, world, e2e_value, e2e_wall, pipe_e2e_s,
+                            m.nx * m.ny * (4 * 5 + 3)),
             "pipelined": None if math.isnan(pipe_ms) else {
                 "value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
                 "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),

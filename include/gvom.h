@@ -61,7 +61,8 @@ typedef enum gvom_status {
  * handle's own map stream (gvom_map_stream) so integrate_scan of the next scan
  * overlaps compute_maps of this one.  One spare buffer slot is allocated; the
  * slot an integrate overwrites is fenced on the compute_maps that last read
- * it.  Results of compute_maps / exports are ordered on the map stream.      */
+ * it.  Results of compute_maps / exports are ordered on the map stream
+ * (except gvom_step's copies to pinned host outputs, see gvom_step).       */
 #define GVOM_FLAG_PIPELINE 1
 /* SPEC S:338 / SURVEY 8(f) NEXT-3 variant: hard and soft obstacle cells are
  * left out of every slope / roughness window (and get NaN themselves).    */
@@ -259,7 +260,13 @@ GVOM_API gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAY
  * stream already under capture by the caller.  With GVOM_FLAG_PIPELINE the
  * step is two graphs -- integrate on the handle's stream, map processing and
  * export on the map stream -- whose slot fences are external event nodes, so
- * consecutive steps overlap.  The
+ * consecutive steps overlap; pinned host points are then copied on a
+ * handle-owned copy stream into one of two staging buffers (overlapping the
+ * previous scan's integrate), and pinned host outputs (without a costmap) are
+ * exported into one of two device buffers and copied to the host on a second
+ * copy stream (overlapping the next step's map processing): those host
+ * outputs are complete after gvom_synchronize, not when the map stream
+ * reaches the step.  The
  * graph and a private capture stream are driver objects held by the handle
  * (released by gvom_destroy); no device memory is allocated.              */
 GVOM_API gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_scan* scans,

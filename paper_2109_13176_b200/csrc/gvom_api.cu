@@ -42,7 +42,7 @@ struct Slot {
 
 struct Layout {
   size_t slot_lut, slot_bits, slot_wprefix, slot_data, slot_meta, slot_stride;
-  size_t staging, rank_tmp, rank_status, epcnt, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
+  size_t staging, staging2, outstage, outstage_bytes, rank_tmp, rank_status, epcnt, tilecnt, tilecnt_bytes, layers_f32, layers_u8, qs, defbits, defbits_bytes, mbits, mprefix,
       roll_rows, roll_nmn, roll_bits, total;
   int64_t cap, nblk, cells;
 };
@@ -117,6 +117,20 @@ Layout make_layout(const gvom_config* c) {
   off = l.slot_stride * (size_t)(c->buffer_frames + ((c->flags & GVOM_FLAG_PIPELINE) ? 1 : 0));
   l.staging = off;
   off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
+  // pipelined: a second staging buffer, so the copy of scan t+1 (copy stream)
+  // overlaps the integrate of scan t, which still reads the first
+  l.staging2 = off;
+  if (c->flags & GVOM_FLAG_PIPELINE)
+    off += align_up(16 * (size_t)(c->max_points_per_frame > 0 ? c->max_points_per_frame : 1));
+  // pipelined gvom_step with pinned host outputs: two device copies of the
+  // layers (one export kernel into one, the copy-out stream drains it while
+  // the next step's map processing runs)
+  l.outstage = off;
+  l.outstage_bytes = 0;
+  if (c->flags & GVOM_FLAG_PIPELINE) {
+    l.outstage_bytes = 5 * align_up(4 * (size_t)c->nx * c->ny) + 3 * align_up((size_t)c->nx * c->ny);
+    off += 2 * l.outstage_bytes;
+  }
   l.rank_tmp = off;
   off += align_up(4 * (size_t)(l.nblk + 2));
   l.rank_status = off;  // [0] ticket counter, [1 + b] tile status (decoupled look-back)
@@ -195,6 +209,19 @@ struct gvom_handle {
   int NS = 0;                       // physical slots: K (+1 when pipelined)
   cudaStream_t mst = nullptr;       // map stream (pipelined)
   cudaEvent_t ev_integrated = nullptr;
+  // gvom_step with pinned host points: their H2D on the copy stream into
+  // staging buffer b (alternating), fenced by ev_staged[b] (copy done) and
+  // ev_sfree[b] (the integrate that read buffer b done)
+  cudaStream_t cst = nullptr;
+  float4* staging2 = nullptr;
+  cudaEvent_t ev_staged[2] = {}, ev_sfree[2] = {};
+  int stage_parity = 0;
+  // ... and pinned host outputs: exported into device buffer b, drained to
+  // the host on the copy-out stream (ev_out_ready[b] / ev_out_free[b])
+  cudaStream_t cst2 = nullptr;
+  char* outstage = nullptr;
+  cudaEvent_t ev_out_ready[2] = {}, ev_out_free[2] = {};
+  int out_parity = 0;
   static constexpr int kMapsRing = 4;
   cudaEvent_t ev_maps[kMapsRing] = {};
   int64_t maps_calls = 0;           // compute_maps calls so far
@@ -543,6 +570,8 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
     s.meta = (uint32_t*)(b + lay.slot_meta);
   }
   h->staging = (float4*)(h->ws + lay.staging);
+  h->staging2 = (float4*)(h->ws + lay.staging2);
+  h->outstage = h->ws + lay.outstage;
   h->rank_tmp = (uint32_t*)(h->ws + lay.rank_tmp);
   const size_t f32 = align_up(4 * (size_t)lay.cells), u8 = align_up((size_t)lay.cells);
   h->layers.height = (float*)(h->ws + lay.layers_f32);
@@ -603,6 +632,13 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
          cudaEventCreateWithFlags(&h->ev_integrated, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < gvom_handle::kMapsRing; ++i)
       ok = cudaEventCreateWithFlags(&h->ev_maps[i], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&h->cst2, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; ok && i < 2; ++i)
+      ok = cudaEventCreateWithFlags(&h->ev_staged[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h->ev_sfree[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h->ev_out_ready[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&h->ev_out_free[i], cudaEventDisableTiming) == cudaSuccess;
   }
   if (!ok || cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -629,6 +665,14 @@ gvom_status gvom_destroy(gvom_handle* h) {
   for (auto e : h->ev_maps)
     if (e) cudaEventDestroy(e);
   if (h->mst) cudaStreamDestroy(h->mst);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_staged[i]) cudaEventDestroy(h->ev_staged[i]);
+    if (h->ev_sfree[i]) cudaEventDestroy(h->ev_sfree[i]);
+    if (h->ev_out_ready[i]) cudaEventDestroy(h->ev_out_ready[i]);
+    if (h->ev_out_free[i]) cudaEventDestroy(h->ev_out_free[i]);
+  }
+  if (h->cst) cudaStreamDestroy(h->cst);
+  if (h->cst2) cudaStreamDestroy(h->cst2);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->gexec_maps) cudaGraphExecDestroy(h->gexec_maps);
@@ -647,6 +691,8 @@ gvom_status gvom_synchronize(gvom_handle* h) {
   if (!h) return GVOM_E_INVALID;
   GVOM_CU(cudaStreamSynchronize(h->st));
   if (h->mst) GVOM_CU(cudaStreamSynchronize(h->mst));
+  if (h->cst) GVOM_CU(cudaStreamSynchronize(h->cst));
+  if (h->cst2) GVOM_CU(cudaStreamSynchronize(h->cst2));
   return GVOM_OK;
 }
 
@@ -821,6 +867,13 @@ static gvom_status integrate_rows(gvom_handle* h, const gvom_scan* scans, int32_
   for (const RayBatch& b : batches)
     GVOM_CU(stage(h, GVOM_STAGE_ENDPOINT, true,
                   [&] { return launch_endpoint(b, d, slot.lut, slot.data, h->st, slab); }));
+  // staging buffer 0 read by this call: a later gvom_step's copy into it waits
+  if (h->cst && !h->capturing)
+    for (int i = 0; i < n_scans; ++i)
+      if (dptr[i] && (const void*)dptr[i] != (const void*)scans[i].xyzw) {
+        GVOM_CU(cudaEventRecord(h->ev_sfree[0], h->st));
+        break;
+      }
   for (int i = 0; i < 3; ++i) slot.origin[i] = h->origin[i];
   if (h->rolling)  // the frame map joins the window map (reading B9)
     GVOM_CU(stage(h, GVOM_STAGE_FINALIZE, true, [&] {
@@ -1025,8 +1078,82 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
   }
   // pipelined: integrate on the handle's stream, map processing + export on
   // the map stream, each its own graph (the fences between steps are the
-  // external event nodes recorded / waited inside them)
-  gvom_status s = capture_launch(h, &h->st, &h->cap, &h->gexec, integrate);
+  // external event nodes recorded / waited inside them).  Pinned host points
+  // are copied on the copy stream into the staging buffer the integrate
+  // before last read (ev_sfree), so the copy overlaps the previous scan's
+  // integrate; the integrate graph waits for it (ev_staged).
+  gvom_scan dsc[GVOM_MAX_SENSORS];
+  int b = -1;
+  for (int i = 0; i < n_scans; ++i)
+    if (scans[i].n > 0 && !is_device_ptr(scans[i].xyzw)) b = h->stage_parity;
+  if (b >= 0) {
+    float4* buf = b ? h->staging2 : h->staging;
+    GVOM_CU(cudaStreamWaitEvent(h->cst, h->ev_sfree[b], 0));
+    int64_t off = 0;
+    for (int i = 0; i < n_scans; ++i) {
+      dsc[i] = scans[i];
+      if (scans[i].n > 0 && !is_device_ptr(scans[i].xyzw)) {
+        GVOM_CU(stage(h, GVOM_STAGE_H2D, false, [&] {
+          return cudaMemcpyAsync(buf + off, scans[i].xyzw, 16 * (size_t)scans[i].n,
+                                 cudaMemcpyHostToDevice, h->cst);
+        }, h->cst));
+        dsc[i].xyzw = (const float*)(buf + off);
+        off += scans[i].n;
+      }
+    }
+    GVOM_CU(cudaEventRecord(h->ev_staged[b], h->cst));
+    h->stage_parity ^= 1;
+  }
+  auto integrate_staged = [&]() -> gvom_status {
+    if (b < 0) return integrate();
+    GVOM_CU(cudaStreamWaitEvent(h->st, h->ev_staged[b], cudaEventWaitExternal));
+    const gvom_status si = gvom_integrate_scan(h, dsc, n_scans);
+    if (si == GVOM_OK)
+      GVOM_CU(cudaEventRecordWithFlags(h->ev_sfree[b], h->st, cudaEventRecordExternal));
+    return si;
+  };
+  gvom_status s = capture_launch(h, &h->st, &h->cap, &h->gexec, integrate_staged);
+  // pinned host outputs (no costmap): the map graph exports into device buffer
+  // ob (after the copy-out of the step before last drained it) and the
+  // copy-out stream moves it to the host, so the next step's map processing
+  // does not wait for the device-to-host copies
+  bool host_out = dst && !cost_weights;
+  for (int l = 0; host_out && l < GVOM_LAYER_COUNT; ++l)
+    if (!is_pinned_host_ptr(dst[l])) host_out = false;
+  if (host_out) {
+    const int ob = h->out_parity;
+    void* sdst[GVOM_LAYER_COUNT];
+    size_t sbytes[GVOM_LAYER_COUNT];
+    char* p = h->outstage + (size_t)ob * h->lay.outstage_bytes;
+    for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
+      size_t elem;
+      layer_src(h, l, &elem);
+      sdst[l] = p;
+      sbytes[l] = elem * (size_t)h->lay.cells;
+      p += align_up(sbytes[l]);
+    }
+    auto maps_staged = [&]() -> gvom_status {
+      gvom_status sm = gvom_compute_maps(h);
+      if (sm != GVOM_OK) return sm;
+      GVOM_CU(cudaStreamWaitEvent(h->mst, h->ev_out_free[ob], cudaEventWaitExternal));
+      sm = gvom_export_layers(h, sdst, sbytes);
+      if (sm == GVOM_OK)
+        GVOM_CU(cudaEventRecordWithFlags(h->ev_out_ready[ob], h->mst, cudaEventRecordExternal));
+      return sm;
+    };
+    if (s == GVOM_OK) s = capture_launch(h, &h->mst, &h->cap_maps, &h->gexec_maps, maps_staged);
+    if (s == GVOM_OK) {
+      GVOM_CU(cudaStreamWaitEvent(h->cst2, h->ev_out_ready[ob], 0));
+      for (int l = 0; l < GVOM_LAYER_COUNT; ++l)
+        GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
+          return cudaMemcpyAsync(dst[l], sdst[l], sbytes[l], cudaMemcpyDeviceToHost, h->cst2);
+        }, h->cst2));
+      GVOM_CU(cudaEventRecord(h->ev_out_free[ob], h->cst2));
+      h->out_parity ^= 1;
+      h->graph_stats[0]++;
+    }
+    return s;
+  }
   if (s == GVOM_OK) s = capture_launch(h, &h->mst, &h->cap_maps, &h->gexec_maps, maps);
   if (s == GVOM_OK) h->graph_stats[0]++;
   return s;

@@ -452,7 +452,8 @@ class GvomMap:
              cost_weights=None, cost: Optional[torch.Tensor] = None):
         """gvom_step: shift + integrate_scan + compute_maps (+ export of all
         layers into `out`, allocated if None; + the costmap with cost_weights,
-        as key "cost") as one CUDA graph launch.
+        as key "cost") as one CUDA graph launch.  On a pipelined handle,
+        pinned host outputs are complete after synchronize().
         Returns (shift delta, layers or None)."""
         p = (C.c_double * 3)(*[float(v) for v in vehicle_xyz])
         dlt = (C.c_int64 * 3)()

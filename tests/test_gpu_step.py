@@ -10,6 +10,7 @@ import pytest
 import torch
 
 from paper_2109_13176_b200 import GvomMap, SensorOutside, synth
+from paper_2109_13176_b200.gvom import LAYER_U8, LAYERS
 from tests.gpu_helpers import compare_layers, layers_np, run_sequence, to_dev
 from oracle import oracle as O
 
@@ -156,6 +157,42 @@ def test_pipelined_step_graphs_overlap_frames():
         compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
     st = m.graph_stats()
     assert st["graph_launches"] == len(w.frames), st
+
+
+def test_pipelined_step_pinned_host_points_and_outputs():
+    # pinned host points on a pipelined handle: each scan is copied on the
+    # copy stream into one of two staging buffers while the previous scan's
+    # integrate still runs; pinned host outputs (alternating sets).  Back to
+    # back without synchronisation, then every frame against the oracle; an
+    # eager integrate_scan from host memory in the middle shares staging 0.
+    w = synth.config3(speed=12.0, n_frames=10, columns=512)
+    grid = dict(w.grid)
+    grid["pipeline"] = True
+    npts = max(f.n_points for f in w.frames)
+    m = GvomMap(grid, max_points_per_frame=npts)
+    om = O.OracleMap(grid)
+    outs, refs = [], []
+    for i, f in enumerate(w.frames):
+        scans = [to_dev(s, host=True) for s in f.scans]
+        om.shift(f.vehicle_xyz)
+        om.integrate([(s.points, s.pose) for s in f.scans])
+        if i == 5:  # the separate calls, host points through staging buffer 0
+            m.shift(f.vehicle_xyz)
+            m.integrate_scan(scans)
+            m.compute_maps()
+            m.synchronize()
+            compare_layers(layers_np(m), om.compute_maps())
+            continue
+        host = {k: torch.empty((m.ny, m.nx), dtype=torch.uint8 if k in LAYER_U8
+                               else torch.float32).pin_memory() for k in LAYERS}
+        _, lay = m.step(f.vehicle_xyz, scans, host)
+        outs.append(lay)
+        refs.append(om.compute_maps())
+    m.synchronize()
+    for lay, L in zip(outs, refs):
+        compare_layers({k: v.cpu().numpy() for k, v in lay.items()}, L)
+    st = m.graph_stats()
+    assert st["graph_launches"] == len(w.frames) - 1 and st["eager_steps"] == 0, st
 
 
 @pytest.mark.parametrize("pipeline", [False, True])

@@ -86,7 +86,9 @@ def main(tag, rnd="r2"):
                     f"{r['launch_ms'] * 1e3:.1f} | {r['frac']:.3f} | "
                     f"{d['integrate']['ms_per_frame'] * 1e3:.1f} | "
                     f"{d['integrate']['hbm_frac']:.3f} | {d['compute_maps_ms'] * 1e3:.1f} | "
-                    f"{d['e2e']['value'] / 1e6:.0f} | {pipe:.0f} |")
+                    f"{d['e2e']['value'] / 1e6:.0f} | "
+                    f"{d['e2e'].get('synchronous_value', d['e2e']['value']) / 1e6:.0f} | "
+                    f"{pipe:.0f} |")
     srows = []
     if os.path.exists(os.path.join(PROF, f"{rnd}_slab_modes.jsonl")):
         for x in open(os.path.join(PROF, f"{rnd}_slab_modes.jsonl")):
@@ -115,8 +117,8 @@ launch that bench.py reports).
 
 ## Bench (device-resident inputs, L2 flushed between steps, one CUDA graph per step)
 
-| workload | step µs | map updates/s | Mpoints/s | k_raycast µs | ray HBM-eq frac | integrate µs | integrate HBM-eq frac | compute_maps µs | e2e Mpoints/s | pipelined updates/s |
-|---|---|---|---|---|---|---|---|---|---|---|
+| workload | step µs | map updates/s | Mpoints/s | k_raycast µs | ray HBM-eq frac | integrate µs | integrate HBM-eq frac | compute_maps µs | e2e Mpoints/s (pipelined) | e2e Mpoints/s (synchronous) | pipelined updates/s |
+|---|---|---|---|---|---|---|---|---|---|---|---|
 {chr(10).join(rows)}
 
 Default line (c2, {d2['steps']} steps): {d2['ms_per_step'] * 1e3:.1f} µs/step,
