@@ -31,18 +31,23 @@ def main():
     ref.compute_maps()
     want = {k: v.cpu().numpy() for k, v in ref.export_layers().items()}
     mine = [s for i, s in enumerate(scans) if i % P == rank]
-    for mode in ("segments", "reduce_scatter", "fused"):
+    for mode in ("segments", "segments_balanced", "reduce_scatter", "fused"):
         m = GvomMap(grid, max_points_per_frame=f.n_points, device=dev)
-        sm = (parallel.SegmentMapper(m) if mode == "segments" else
+        sm = (parallel.SegmentMapper(m) if mode.startswith("segments") else
               parallel.SlabMapper(m, ep_capacity=f.n_points, fused=(mode == "fused")))
         m.shift(f.vehicle_xyz)
         sm.integrate(mine)
         sm.compute_maps()
+        if mode == "segments_balanced":  # bounds from this frame's row work, then again
+            sm.rebalance()
+            m.shift(f.vehicle_xyz)
+            sm.integrate(mine)
+            sm.compute_maps()
         lay = m.export_layers()
         m.synchronize()
         for k in LAYERS:
             t = lay[k].contiguous()
-            parallel.gather_rows(t, sm.y0, sm.y1)
+            parallel.gather_rows(t, sm.y0, sm.y1, None, sm.ys)
             got = t.cpu().numpy()
             if k in ("slope", "roughness", "spread"):
                 ok = np.array_equal(np.isnan(got), np.isnan(want[k]))

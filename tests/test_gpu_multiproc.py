@@ -26,5 +26,5 @@ def test_partitioned_path_two_gpus(config):
                         "--master-port", str(29700 + config), os.path.join(HERE, "multi_gpu_worker.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    for mode in ("segments", "reduce_scatter", "fused", "segments_motion"):
+    for mode in ("segments", "segments_balanced", "reduce_scatter", "fused", "segments_motion"):
         assert f"MULTI-GPU {mode} P={P} ok" in r.stdout
