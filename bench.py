@@ -54,6 +54,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 # stdout carries exactly one JSON line: keep NCCL's banner ("NCCL version ...") off it
 os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # its version banner too
 
 METRIC = "lidar points/s integrated and map updates/s (256×256×64), % HBM roofline"
 L2_FLUSH_BYTES = 256 << 20

@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_step.py tests/test_gpu_parity.py -x -q -k "step or pipelin or c2_single" > gpurun_out/t27.log 2>&1; echo tests rc=$?; grep -E "assert |FAILED|Error" gpurun_out/t27.log | head -5; tail -1 gpurun_out/t27.log
-for c in 1 2 3; do timeout 600 python bench.py --config $c --steps 100 --no-partitioned --no-cpu-baseline --no-l2-probe 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());e=d['e2e'];print('E2E', d['config']['workload'][:3], 'step', round(d['ms_per_step']*1e3,1), 'e2e %.0f'%(e['value']/1e6), e['mode'], 'sync %.0f'%(e['synchronous_value']/1e6), 'wall %.0f'%(e['synchronous_wall_value']/1e6), 'pipe_dev', d['pipelined']['map_updates_per_s'])"; done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=1 --master-addr 127.0.0.1 --master-port 29733 tools/slab_step_parts.py 2>/dev/null | tail -1
+for r in 1 2; do timeout 600 python bench.py --slab --config 4 --slab-mode segments --steps 20 --warmup 3 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('SLAB', d['ms_per_step'])"; done
+timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random.py tests/test_gpu_step.py tests/test_gpu_rolling.py tests/test_gpu_shapes.py -x -q > gpurun_out/t29.log 2>&1; echo tests rc=$?; grep -E "assert |FAILED|Error" gpurun_out/t29.log | head -5; tail -1 gpurun_out/t29.log
+bash tools/ab_env.sh "1 2 3" "- GVOM_EP_FUSED=0" 50 2>&1 | tee gpurun_out/ab29.log
