@@ -250,6 +250,9 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
   k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
 }
 
+#ifndef GVOM_RAY_STREAM_PREFIX
+#define GVOM_RAY_STREAM_PREFIX 1
+#endif
 #ifndef GVOM_RAY_UNROLL
 #define GVOM_RAY_UNROLL 1
 #endif
@@ -259,6 +262,16 @@ template <bool kStream, bool kNeg, class Step>
 __device__ __forceinline__ void walk_loop(uint32_t* __restrict__ miss, const uint32_t& L, int left,
                                           int lane, unsigned after_lanes, Step&& step) {
   if (kStream) {
+    // the first Tmin steps have every lane active: no per-step ballot
+    // (GVOM_RAY_STREAM_PREFIX=0: without this prefix, A/B builds)
+#if GVOM_RAY_STREAM_PREFIX
+    const int Tmin = __reduce_min_sync(0xffffffffu, left);
+    for (int it = 0; it < Tmin; ++it) {
+      aggregate_red_stream<kNeg>(miss, L, true, 0xffffffffu, after_lanes, lane);
+      step();
+    }
+    left -= Tmin;
+#endif
     unsigned act = __ballot_sync(0xffffffffu, left > 0);
     while (act) {
       const bool active = left > 0;
