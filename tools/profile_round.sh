@@ -42,3 +42,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ra
   -o $out/full_c5_raycast python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline --no-partitioned \
   > $out/full_c5.log 2>&1
 echo "full c5 rc=$?"
+# 7. the partitioned path's per-rank cost, P ranks emulated on one GPU (c5)
+timeout 1200 python tools/slab_scaling.py 4 > $out/slab_scaling.json 2> $out/slab_scaling.log
+echo "slab scaling rc=$?"

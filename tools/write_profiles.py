@@ -41,6 +41,12 @@ def main(tag, rnd="r2"):
     for f in ("launches.csv", "bench_configs.jsonl", "slab_modes.jsonl"):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(PROF, f"{rnd}_{f}"))
+    scal = None
+    if os.path.exists(os.path.join(src, "slab_scaling.json")):
+        txt = [x for x in open(os.path.join(src, "slab_scaling.json")) if x.startswith("{")]
+        if txt:
+            scal = json.loads(txt[-1])
+            json.dump(scal, open(os.path.join(PROF, f"{rnd}_slab_scaling_emulated.json"), "w"))
     line = [x for x in open(os.path.join(src, "bench_c2.json")).read().strip().splitlines()
             if x.startswith("{")][-1]
     open(os.path.join(PROF, f"{rnd}_bench_c2.json"), "w").write(line + "\n")
@@ -104,6 +110,23 @@ def main(tag, rnd="r2"):
         f"{v['runs_of_4']['g_l2_requests_s']:.0f} G req/s" for k, v in l2.items()
         if v.get("random_word") and v.get("runs_of_4"))
     rr = ray2.get("raycast_red") or {}
+    scal_md = ""
+    if scal:
+        lines_ = []
+        for P in sorted(scal["segments"], key=int):
+            a, b, c = scal["segments"][P], scal["segments_balanced"][P], scal["reduce_scatter"][P]
+            lines_.append(f"| {P} | {a['max_ms']:.2f} / {a['mean_ms']:.2f} | "
+                          f"{b['max_ms']:.2f} / {b['mean_ms']:.2f} | {c['max_ms']:.2f} | "
+                          f"{scal['segments_balanced']['1']['max_ms'] / b['max_ms']:.2f} |")
+        scal_md = f"""
+## P ranks emulated on one GPU (c5; `{rnd}_slab_scaling_emulated.json`, tools/slab_scaling.py)
+
+Each rank's calls timed alone; max / mean over ranks, collectives not included.
+
+| P | ray segments, equal rows: max / mean ms | ray segments, balanced: max / mean ms | reduce-scatter compute: max ms | speed-up of balanced max vs P = 1 |
+|---|---|---|---|---|
+{chr(10).join(lines_)}
+"""
     md = f"""# Round 2 profile summary (B200, sm_100a)
 
 Regenerated by `tools/profile_round.sh {tag}` (under gpurun, 1 GPU; every ncu command ran
@@ -133,10 +156,10 @@ The ray cast: {rr.get('g_l2_requests_s') or float('nan'):.0f} G L2 reduction req
 
 ## Partitioned path on one rank (c5; `{rnd}_slab_modes.jsonl`)
 
-| mode | ranks | ms/frame | Mpoints/s |
+| mode | ranks | µs/frame | Mpoints/s |
 |---|---|---|---|
 {chr(10).join(srows)}
-
+{scal_md}
 ## Launch list (`{rnd}_launches.csv`, c2, cold caches, serialised)
 
 ```
