@@ -250,6 +250,9 @@ __device__ __forceinline__ void dda_step(float& k0, float& k1, float& k2, float&
   k2 = __fmul_rn(__fsub_rn(e2, s2), i2);
 }
 
+#ifndef GVOM_RESET_V8
+#define GVOM_RESET_V8 1  // k_reset_slot with 32-byte stores (A/B builds: 0 = 16-byte)
+#endif
 #ifndef GVOM_RAY_STREAM_PREFIX
 #define GVOM_RAY_STREAM_PREFIX 1
 #endif
@@ -986,6 +989,35 @@ __global__ void __launch_bounds__(256) k_reset_slot(int32_t* __restrict__ lut, i
   const int4 ones = make_int4(-1, -1, -1, -1);
   int4* l4 = reinterpret_cast<int4*>(lut + l0);
   int64_t i = i0;
+#if GVOM_RESET_V8
+  {  // 32-byte stores (STG.256; l0 is a tile start: 32 KB aligned), four in flight
+    const int64_t n8 = n4 >> 1;
+    char* l8 = reinterpret_cast<char*>(lut + l0);
+    int64_t k = i0;
+    for (; k + 3 * stride < n8; k += 4 * stride) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        char* a = l8 + 32 * (k + u * stride);
+        if (kKeep)
+          asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(a), "r"(-1)
+                       : "memory");
+        else
+          asm volatile("st.global.cs.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(a), "r"(-1)
+                       : "memory");
+      }
+    }
+    for (; k < n8; k += stride) {
+      char* a = l8 + 32 * k;
+      if (kKeep)
+        asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(a), "r"(-1)
+                     : "memory");
+      else
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(a), "r"(-1)
+                     : "memory");
+    }
+    i = 2 * n8 + i0;  // the odd 16-byte chunk, if any, below
+  }
+#endif
   for (; i + 3 * stride < n4; i += 4 * stride) {  // four 16-byte stores in flight
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
