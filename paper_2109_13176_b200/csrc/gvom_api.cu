@@ -348,22 +348,61 @@ void roll_set_origin(RollGrid& g, const gvom_config& c, const int64_t o[3]) {
   g.zo = pm(o[2], c.nz);
 }
 
-bool is_pinned_host_ptr(const void* p) {
-  cudaPointerAttributes attr;
-  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+// Memory type of a pointer (cudaPointerGetAttributes).  Within one gvom_step
+// call (MemoScope) the answers are memoised -- the call checks the same scan
+// and output pointers several times, and the caller keeps every buffer valid
+// for the duration of the call -- and the handle's own workspace is device
+// memory without asking.
+struct PtrMemo {
+  static constexpr int kN = 48;
+  const void* p[kN];
+  int t[kN];
+  int n = 0;
+  const char* ws0 = nullptr;
+  const char* ws1 = nullptr;
+  bool on = false;
+};
+thread_local PtrMemo g_memo;
+
+struct MemoScope {
+  explicit MemoScope(const gvom_handle* h) {
+    g_memo.on = true;
+    g_memo.n = 0;
+    g_memo.ws0 = h->ws;
+    g_memo.ws1 = h->ws + h->lay.total;
   }
-  return attr.type == cudaMemoryTypeHost;
+  ~MemoScope() {
+    g_memo.on = false;
+    g_memo.n = 0;
+  }
+};
+
+int mem_type(const void* p) {
+  if (g_memo.on) {
+    const char* c = (const char*)p;
+    if (c >= g_memo.ws0 && c < g_memo.ws1) return cudaMemoryTypeDevice;
+    for (int i = 0; i < g_memo.n; ++i)
+      if (g_memo.p[i] == p) return g_memo.t[i];
+  }
+  int t = cudaMemoryTypeUnregistered;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess)
+    cudaGetLastError();
+  else
+    t = (int)attr.type;
+  if (g_memo.on && g_memo.n < PtrMemo::kN) {
+    g_memo.p[g_memo.n] = p;
+    g_memo.t[g_memo.n] = t;
+    g_memo.n++;
+  }
+  return t;
 }
 
+bool is_pinned_host_ptr(const void* p) { return mem_type(p) == cudaMemoryTypeHost; }
+
 bool is_device_ptr(const void* p) {
-  cudaPointerAttributes attr;
-  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+  const int t = mem_type(p);
+  return t == cudaMemoryTypeDevice || t == cudaMemoryTypeManaged;
 }
 
 #define GVOM_CU(x)                                     \
@@ -1014,6 +1053,7 @@ gvom_status gvom_step(gvom_handle* h, const double vehicle_xyz[3], const gvom_sc
                       void* cost_dst, size_t cost_bytes, int64_t out_delta[3]) {
   NvtxRange nvtx_("gvom_step");
   if (!h || !vehicle_xyz) return GVOM_E_INVALID;
+  MemoScope memo_(h);
   if (dst && !dst_bytes) return GVOM_E_INVALID;
   if ((cost_weights == nullptr) != (cost_dst == nullptr)) return GVOM_E_INVALID;
   if (cost_weights) {
