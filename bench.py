@@ -503,6 +503,29 @@ def pipelined_ms(w, frames, dev_frames, npts, dev, stream, out, args, barrier):
     return ms
 
 
+def pcie_probe(dev, h2d_bytes: int, d2h_bytes: int, reps: int = 20):
+    """Host<->device copy bandwidth of this box for the step's own transfer
+    sizes (pinned host memory, CUDA events): the e2e number's ceiling."""
+    import torch
+    out = {}
+    for name, nbytes, to_dev in (("h2d", h2d_bytes, True), ("d2h", d2h_bytes, False)):
+        h = torch.empty(max(nbytes, 16), dtype=torch.uint8).pin_memory()
+        d = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                (d.copy_(h, non_blocking=True) if to_dev else h.copy_(d, non_blocking=True))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(reps):
+                (d.copy_(h, non_blocking=True) if to_dev else h.copy_(d, non_blocking=True))
+            b.record(s)
+        b.synchronize()
+        out[f"{name}_gbs"] = nbytes * reps / (a.elapsed_time(b) / 1e3) / 1e9
+    out["bytes"] = {"h2d": h2d_bytes, "d2h": d2h_bytes}
+    return out
+
+
 def e2e_line(npts, steps, world, sync_value, sync_wall_s, pipe_s, d2h_bytes):
     """The e2e object: a user's stream of scans through gvom_step with pinned
     host buffers -- H2D of every scan and D2H of every step's 8 layers inside
@@ -780,8 +803,9 @@ def main():
             "stages_ms_per_step": {s: v[0] / n_inst for s, v in stage_all.items() if v[1]},
             "stages_note": "separate instrumented pass (events around every launch, "
                            "separate calls without a graph)",
-            "e2e": e2e_line(npts, e2e_steps, world, e2e_value, e2e_wall, pipe_e2e_s,
-                            m.nx * m.ny * (4 * 5 + 3)),
+            "e2e": dict(e2e_line(npts, e2e_steps, world, e2e_value, e2e_wall, pipe_e2e_s,
+                                 m.nx * m.ny * (4 * 5 + 3)),
+                        pcie=pcie_probe(dev, 16 * npts, m.nx * m.ny * (4 * 5 + 3))),
             "pipelined": None if math.isnan(pipe_ms) else {
                 "value": pts_total / (pipe_ms / 1e3), "unit": "points/s",
                 "map_updates_per_s": world * args.steps / (pipe_ms / 1e3),
