@@ -152,8 +152,15 @@ __device__ __forceinline__ void write_column(const LayerPtrs& out, const LayerPa
 //          lane sums its own map's hits / hits+misses over them with no
 //          cross-lane traffic; only the two edge voxels need the merged
 //          min_dz (a group min).  One group sum at the end.
+// k_columns' min resident blocks per SM: 6 (40 registers, 16 bytes spilled)
+// gives 888 resident blocks instead of 740 for a grid of 1024 (c2) -- the
+// second partial wave shrinks: c2 columns 28.0 vs 29.0 us, c4 57.0 vs 63.4 us
+// (instrumented, same box); 8 (32 registers) spills more and gains less
+#ifndef GVOM_COL_MINB
+#define GVOM_COL_MINB 6
+#endif
 template <bool kEarlyEdges>
-__global__ void __launch_bounds__(256) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
+__global__ void __launch_bounds__(256, GVOM_COL_MINB) k_columns(const __grid_constant__ SlotSet ss, const Dims d,
                                                  const LayerParams lp, const LayerPtrs out,
                                                  int64_t cbeg, int64_t cells) {
   const int lane = threadIdx.x & 31;
