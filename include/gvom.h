@@ -162,6 +162,8 @@ GVOM_API size_t gvom_workspace_bytes(const gvom_config* cfg);
  * The initial origin is the snap of vehicle (0,0,0).                       */
 GVOM_API gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_bytes,
                         void* cuda_stream, gvom_handle** out);
+/* gvom_destroy waits for the handle's work (its stream and internal streams)
+ * before releasing its driver objects, so the workspace may be freed after. */
 GVOM_API gvom_status gvom_destroy(gvom_handle* h);
 GVOM_API gvom_status gvom_set_stream(gvom_handle* h, void* cuda_stream);
 GVOM_API gvom_status gvom_synchronize(gvom_handle* h);

@@ -692,6 +692,12 @@ gvom_status gvom_create(const gvom_config* cfg, void* d_workspace, size_t ws_byt
 
 gvom_status gvom_destroy(gvom_handle* h) {
   if (!h) return GVOM_E_INVALID;
+  // the caller frees the workspace next: let the handle's own streams drain
+  // first (the copy, planner and map streams may still be using it)
+  cudaStreamSynchronize(h->st);  // (null: the legacy default stream)
+  for (cudaStream_t s : {h->mst, h->aux, h->cst, h->cst2})
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
   for (auto& r : h->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
