@@ -624,8 +624,11 @@ __device__ __forceinline__ void ray_warp(const RayBatch& rb, const Dims& d,
 // kNeg: misses count down from -1 in the slot's LUT (the integrate path, see
 // k_finalize_lut); else up from 0 in a plain miss grid (the multi-GPU partial
 // grids that are reduce-scattered).
+#ifndef GVOM_RAY_MINB64
+#define GVOM_RAY_MINB64 1  // min resident 64-thread ray-cast blocks per SM (A/B builds)
+#endif
 template <bool kStream, int kBS, bool kNeg>
-__global__ void __launch_bounds__(kBS, 1) k_raycast(const __grid_constant__ RayBatch rb,
+__global__ void __launch_bounds__(kBS, kBS == 64 ? GVOM_RAY_MINB64 : 1) k_raycast(const __grid_constant__ RayBatch rb,
                                                  const Dims d, uint32_t* __restrict__ miss,
                                                  uint32_t* __restrict__ bits,
                                                  const TileCounts tc, bool last_sensor) {
