@@ -221,3 +221,26 @@ def test_step_capture_failure_rolls_back(pipeline):
     lut, data, origin = m.export_frame(1)
     assert np.array_equal(origin, om.buffer[-2].origin)
     assert np.array_equal(lut, om.buffer[-2].lut)
+
+
+def test_destroy_with_pipelined_work_in_flight():
+    # gvom_destroy drains the handle's streams (integrate, map, copy streams)
+    # before releasing, so freeing the workspace right after is safe: steps are
+    # submitted back to back with pinned host buffers, the handle is closed
+    # without a synchronise, its workspace dropped, and a fresh handle then
+    # reproduces the oracle on the same memory pool
+    w = synth.config3(speed=12.0, n_frames=4, columns=512)
+    grid = dict(w.grid)
+    grid["pipeline"] = True
+    npts = max(f.n_points for f in w.frames)
+    for _ in range(3):
+        m = GvomMap(grid, max_points_per_frame=npts)
+        for f in w.frames:
+            host = {k: torch.empty((m.ny, m.nx), dtype=torch.uint8 if k in LAYER_U8
+                                   else torch.float32).pin_memory() for k in LAYERS}
+            m.step(f.vehicle_xyz, [to_dev(s, host=True) for s in f.scans], host)
+        m.close()
+        del m
+        torch.cuda.empty_cache()
+    run_sequence(w, use_step=True, check_every=2)
+

@@ -226,6 +226,15 @@ def _worker_segments(rank, world, port, q):
         got2 = parallel.all_gather_points(mine, meta)
         for (p, pose, rings), (pr, poser) in zip(got2, scans):
             assert np.array_equal(p.numpy(), pr) and np.array_equal(pose, poser) and rings == 16
+        # with buffers kept across frames (SegmentMapper): a second frame with
+        # other points reuses them and still gathers exactly
+        bufs = {}
+        parallel.all_gather_points(mine, meta, None, bufs)
+        mine2 = [(torch.from_numpy(scans[rank][0] * 2.0), scans[rank][1], 16)]
+        got3 = parallel.all_gather_points(mine2, meta, None, bufs)
+        assert bufs["cap"] >= max(s[0].shape[0] for s in scans)
+        for (p, pose, rings), (pr, poser) in zip(got3, scans):
+            assert np.array_equal(p.numpy(), pr * 2.0) and rings == 16
         dims = (grid["nx"], grid["ny"], grid["nz"])
         nx, ny, nz = dims
         res = grid["res"]
