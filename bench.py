@@ -54,7 +54,25 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 # stdout carries exactly one JSON line: keep NCCL's banner ("NCCL version ...") off it
 os.environ.setdefault("NCCL_DEBUG", "WARN")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # its version banner too
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_OUT = None
+
+
+def _stdout_to_stderr():
+    """Everything any library writes to stdout (NCCL prints its version banner
+    there at communicator creation whatever NCCL_DEBUG_FILE says) goes to
+    stderr; the JSON line is written to the real stdout by emit()."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 METRIC = "lidar points/s integrated and map updates/s (256×256×64), % HBM roofline"
 L2_FLUSH_BYTES = 256 << 20
@@ -340,7 +358,7 @@ def run_reference(args):
         "e2e": {"value": r["value"], "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -466,7 +484,7 @@ def main_slab(args):
     line = slab_measure(cfg, args.steps, args.warmup, args.slab_mode,
                         balance=not args.no_balance)
     if line is not None:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.barrier()
     dist.destroy_process_group()
     return 0
@@ -580,6 +598,7 @@ def pipelined_e2e_s(w, frames, host_frames, host_outs, npts, dev, stream, steps,
 
 
 def main():
+    _stdout_to_stderr()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -826,7 +845,7 @@ def main():
                             "(the N = 1 point of `bench.py --gpus N`, N > 1)")
             line["partitioned"] = part
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
