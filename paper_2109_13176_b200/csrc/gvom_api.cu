@@ -189,6 +189,9 @@ struct gvom_handle {
   int64_t origin[3] = {0, 0, 0};
   int64_t map_origin[3] = {0, 0, 0};
   bool maps_valid = false;
+  // the negative layer's per-cell decision deferred into the export (whole-map
+  // sweeps): pending until an export / costmap needs it (ensure_neg)
+  bool neg_pending = false;
   SlotSet map_slots{};
   bool timing = false;
   std::vector<TimedRec> recs;
@@ -463,6 +466,7 @@ struct HostState {
   bool maps_valid = false;
   SlotSet map_slots{};
   uint64_t rank_calls = 0;
+  bool neg_pending = false;
 };
 
 HostState save_state(const gvom_handle* h) {
@@ -477,6 +481,7 @@ HostState save_state(const gvom_handle* h) {
   s.maps_valid = h->maps_valid;
   s.map_slots = h->map_slots;
   s.rank_calls = h->rank_calls;
+  s.neg_pending = h->neg_pending;
   return s;
 }
 
@@ -492,6 +497,7 @@ void restore_state(gvom_handle* h, const HostState& s) {
   h->maps_valid = s.maps_valid;
   h->map_slots = s.map_slots;
   h->rank_calls = s.rank_calls;
+  h->neg_pending = s.neg_pending;
 }
 
 // Capture body()'s launches with *role (h->st or h->mst) redirected to a
@@ -953,12 +959,23 @@ static cudaError_t surface_layers(gvom_handle* h) {
   cudaError_t e = cudaEventRecord(h->ev_fork, h->ms());
   if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
   if (e == cudaSuccess && h->lp.neg_8cone) {
+    h->neg_pending = false;
     e = stage(h, GVOM_STAGE_NEGATIVE, true,
               [&] { return launch_negative8(h->d, h->lp, h->layers, h->aux); }, h->aux);
   } else if (e == cudaSuccess) {
+    // whole map: the per-cell decision (k_neg_decide) is made by the export,
+    // after the join, which reads the sweeps' min / max on its way (ensure_neg
+    // for the other consumers); GVOM_NEG_DEFER=0 decides here (A/B)
+    static int defer_env = -1;
+    if (defer_env < 0) {
+      const char* ev = getenv("GVOM_NEG_DEFER");
+      defer_env = ev ? (atoi(ev) ? 1 : 0) : 1;
+    }
+    const bool defer = defer_env && h->lp.row0 == 0 && h->lp.row1 == h->cfg.ny;
     e = stage(h, GVOM_STAGE_NEGATIVE, true,
-              [&] { return launch_negative(h->d, h->lp, h->layers, h->aux); }, h->aux);
-    if (e == cudaSuccess) h->launches++;  // k_neg_decide
+              [&] { return launch_negative(h->d, h->lp, h->layers, h->aux, !defer); }, h->aux);
+    if (e == cudaSuccess && !defer) h->launches++;  // k_neg_decide
+    h->neg_pending = e == cudaSuccess && defer;
   }
   if (e == cudaSuccess)
     e = stage(
@@ -1003,6 +1020,20 @@ gvom_status gvom_compute_maps(gvom_handle* h) {
   return GVOM_OK;
 }
 
+// A deferred negative decision, before anything other than the one-kernel
+// export reads the negative layer (whole map: rows 0..ny).
+static cudaError_t ensure_neg(gvom_handle* h) {
+  if (!h->neg_pending) return cudaSuccess;
+  LayerParams lp = h->lp;
+  lp.row0 = 0;
+  lp.row1 = h->cfg.ny;
+  const cudaError_t e = stage(
+      h, GVOM_STAGE_NEGATIVE, true, [&] { return launch_neg_decide(h->d, lp, h->layers, h->ms()); },
+      h->ms());
+  if (e == cudaSuccess) h->neg_pending = false;
+  return e;
+}
+
 static const void* layer_src(gvom_handle* h, int layer, size_t* elem) {
   *elem = 4;
   switch (layer) {
@@ -1034,11 +1065,25 @@ gvom_status gvom_export_layers(gvom_handle* h, void* const dst[GVOM_LAYER_COUNT]
     if (dst_bytes[l] < (size_t)job.bytes[l]) return GVOM_E_SIZE;
     if (((uintptr_t)dst[l] & 15) != 0 || !is_device_ptr(dst[l])) one_kernel = false;
   }
-  if (one_kernel) {
+  if (one_kernel) {  // (with a deferred negative decision made on the way)
+    NegDecide dec{};
+    if (h->neg_pending && ((uintptr_t)dst[GVOM_LAYER_NEGATIVE] & 3) == 0) {
+      dec.qs = h->layers.qs;
+      dec.nmin = h->layers.nmin;
+      dec.nmax = h->layers.nmax;
+      dec.neg = h->layers.neg;
+      dec.T_neg = h->lp.T_neg;
+      dec.on = true;
+    } else {
+      GVOM_CU(ensure_neg(h));
+    }
     GVOM_CU(stage(
-        h, GVOM_STAGE_EXPORT, true, [&] { return launch_export_layers(job, h->ms()); }, h->ms()));
+        h, GVOM_STAGE_EXPORT, true, [&] { return launch_export_layers(job, h->ms(), dec); },
+        h->ms()));
+    h->neg_pending = false;
     return GVOM_OK;
   }
+  GVOM_CU(ensure_neg(h));
   for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {
     GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
       return cudaMemcpyAsync(job.dst[l], job.src[l], (size_t)job.bytes[l], cudaMemcpyDefault,
@@ -1226,6 +1271,7 @@ gvom_status gvom_export_2d(gvom_handle* h, gvom_layer layer, void* dst, size_t d
   if (!src) return GVOM_E_INVALID;
   const size_t bytes = elem * (size_t)h->lay.cells;
   if (dst_bytes < bytes) return GVOM_E_SIZE;
+  if (layer == GVOM_LAYER_NEGATIVE) GVOM_CU(ensure_neg(h));
   GVOM_CU(stage(h, GVOM_STAGE_EXPORT, false, [&] {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->ms());
   }));
@@ -1245,6 +1291,7 @@ gvom_status gvom_costmap(gvom_handle* h, const float weights[7], void* dst, size
   }
   const bool direct = is_device_ptr(dst) && ((uintptr_t)dst & 3) == 0;
   float* out = direct ? (float*)dst : h->layers.cost;
+  GVOM_CU(ensure_neg(h));
   GVOM_CU(stage(
       h, GVOM_STAGE_EXPORT, true,
       [&] { return launch_costmap(h->d, h->layers, cw, out, h->ms()); }, h->ms()));
@@ -1265,6 +1312,7 @@ gvom_status gvom_export_layers_cost(gvom_handle* h, void* const dst[GVOM_LAYER_C
     cw.w[i] = weights[i];
   }
   if (cost_bytes < 4 * (size_t)h->lay.cells) return GVOM_E_SIZE;
+  GVOM_CU(ensure_neg(h));
   CopyJob job;
   bool fused = is_device_ptr(cost_dst) && ((uintptr_t)cost_dst & 3) == 0;
   for (int l = 0; l < GVOM_LAYER_COUNT; ++l) {

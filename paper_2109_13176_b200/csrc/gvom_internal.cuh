@@ -280,7 +280,7 @@ cudaError_t launch_transpose_init(const Dims& d, const LayerParams& lp, const La
 cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
                          cudaStream_t st);
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
-                            cudaStream_t st);  // cone sweeps -> nmin / nmax (slope writes neg)
+                            cudaStream_t st, bool decide = true);  // cone sweeps -> nmin / nmax (slope writes neg)
 cudaError_t launch_merge_bits(const SlotSet& ss, const Dims& d, uint32_t* mbits, cudaStream_t st);
 cudaError_t launch_merge_write(const SlotSet& ss, const Dims& d, const uint32_t* mbits,
                                const uint32_t* mprefix, int32_t* lut, gvom_voxel* data,
@@ -291,7 +291,22 @@ struct CopyJob {
   void* dst[GVOM_LAYER_COUNT];
   int64_t bytes[GVOM_LAYER_COUNT];
 };
-cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st);
+// dec.on: the negative layer (job index GVOM_LAYER_NEGATIVE) is decided from
+// the cone sweeps' min / max while it is exported (k_neg_decide fused into
+// the export: written to job.dst and to dec.neg)
+struct NegDecide {
+  const int32_t* qs = nullptr;
+  const int32_t* nmin = nullptr;
+  const int32_t* nmax = nullptr;
+  uint8_t* neg = nullptr;
+  int64_t T_neg = 0;
+  bool on = false;
+};
+cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st,
+                                 const NegDecide& dec = NegDecide{});
+// k_neg_decide alone over rows [lp.row0, lp.row1) (a deferred decision)
+cudaError_t launch_neg_decide(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                              cudaStream_t st);
 struct CostWeights {
   float w[7];  // hard, soft, density, negative, slope, roughness, unknown
 };

@@ -1289,8 +1289,38 @@ __global__ void __launch_bounds__(256) k_merge_write(const SlotSet ss, const Dim
 }
 
 // All 2D layers in one launch: blockIdx.y selects the layer; 16-byte chunks.
-__global__ void __launch_bounds__(256) k_export_layers(const __grid_constant__ CopyJob job) {
+__device__ __forceinline__ uint32_t neg_decision(const NegDecide& dec, int32_t q, int32_t mn,
+                                                 int32_t mx) {
+  return (q == kQsUndef && mx != INT32_MIN && (int64_t)mx - (int64_t)mn > dec.T_neg) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_export_layers(const __grid_constant__ CopyJob job,
+                                                       const __grid_constant__ NegDecide dec) {
   const int l = blockIdx.y;
+  if (dec.on && l == GVOM_LAYER_NEGATIVE) {
+    // k_neg_decide's rule on the way out: four cells per thread, 16-byte loads
+    // of q_s / nmin / nmax, one 4-byte store to the caller and to the layer
+    const int64_t n = job.bytes[l], n4 = n >> 2;
+    const int4* q4 = reinterpret_cast<const int4*>(dec.qs);
+    const int4* a4 = reinterpret_cast<const int4*>(dec.nmin);
+    const int4* b4 = reinterpret_cast<const int4*>(dec.nmax);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int4 q = __ldcs(q4 + i), a = __ldcs(a4 + i), b = __ldcs(b4 + i);
+      const uint32_t v = neg_decision(dec, q.x, a.x, b.x) | neg_decision(dec, q.y, a.y, b.y) << 8 |
+                         neg_decision(dec, q.z, a.z, b.z) << 16 |
+                         neg_decision(dec, q.w, a.w, b.w) << 24;
+      reinterpret_cast<uint32_t*>(job.dst[l])[i] = v;
+      reinterpret_cast<uint32_t*>(dec.neg)[i] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+      const int64_t c = (n4 << 2) + threadIdx.x;
+      const uint8_t v = (uint8_t)neg_decision(dec, dec.qs[c], dec.nmin[c], dec.nmax[c]);
+      reinterpret_cast<uint8_t*>(job.dst[l])[c] = v;
+      dec.neg[c] = v;
+    }
+    return;
+  }
   const int64_t n16 = job.bytes[l] >> 4;
   const uint4* __restrict__ src = reinterpret_cast<const uint4*>(job.src[l]);
   uint4* __restrict__ dst = reinterpret_cast<uint4*>(job.dst[l]);
@@ -1367,7 +1397,7 @@ cudaError_t launch_slope(const Dims& d, const LayerParams& lp, const LayerPtrs& 
 inline bool neg_tb_enabled() { return GVOM_NEG_TB != 0; }  // A/B knob
 
 cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool decide) {
   const int A = d.nx > d.ny ? d.nx : d.ny, B = A;  // smem sized for the longest line
   const int K = lp.neg_cells;
   // tiles: about one block per SM over the emitted lines of the 4 cones (rows
@@ -1431,10 +1461,8 @@ cudaError_t launch_negative(const Dims& d, const LayerParams& lp, const LayerPtr
     k_negative<<<grid, nthr + 32, smem, st>>>(d, lp, out, T, R);
   }
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const int64_t dc = (int64_t)(lp.row1 - lp.row0) * d.nx;
-  k_neg_decide<<<(unsigned)((dc + 255) / 256), 256, 0, st>>>(d, lp, out);
-  return cudaGetLastError();
+  if (e != cudaSuccess || !decide) return e;
+  return launch_neg_decide(d, lp, out, st);
 }
 
 cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
@@ -1464,13 +1492,21 @@ cudaError_t launch_negative8(const Dims& d, const LayerParams& lp, const LayerPt
   return cudaGetLastError();
 }
 
-cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st) {
+cudaError_t launch_export_layers(const CopyJob& job, cudaStream_t st, const NegDecide& dec) {
   int64_t mx = 0;
   for (int l = 0; l < GVOM_LAYER_COUNT; ++l) mx = job.bytes[l] > mx ? job.bytes[l] : mx;
   int64_t blocks = ((mx >> 4) + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 4) blocks = 148 * 4;
-  k_export_layers<<<dim3((unsigned)blocks, GVOM_LAYER_COUNT), 256, 0, st>>>(job);
+  k_export_layers<<<dim3((unsigned)blocks, GVOM_LAYER_COUNT), 256, 0, st>>>(job, dec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_neg_decide(const Dims& d, const LayerParams& lp, const LayerPtrs& out,
+                              cudaStream_t st) {
+  const int64_t dc = (int64_t)(lp.row1 - lp.row0) * d.nx;
+  if (dc <= 0) return cudaSuccess;
+  k_neg_decide<<<(unsigned)((dc + 255) / 256), 256, 0, st>>>(d, lp, out);
   return cudaGetLastError();
 }
 
