@@ -3,7 +3,9 @@ maps bit for bit too, so an A/B timing never compares a wrong kernel:
 
 * GVOM_COL_FAST=1   -- k_columns_fast (three round trips per column);
 * GVOM_SLOPE_COMPACT=1 -- k_slope_c over the compacted column list;
-* GVOM_COL_EARLY=1  -- k_columns<true> (edge loads issued first).
+* GVOM_COL_EARLY=1  -- k_columns<true> (edge loads issued first);
+* GVOM_NEG_DEFER=0  -- the negative decision right after the cone sweep
+  (k_neg_decide) instead of inside the export.
 
 The switches are read once per process, so each set runs the parity tests in
 a child process (as test_gpu_split.py does for the split ray cast)."""
@@ -25,8 +27,8 @@ TESTS = ["test_gpu_parity.py::test_c1_tiny", "test_gpu_parity.py::test_c2_single
 
 @pytest.mark.parametrize("switches", [
     {"GVOM_COL_FAST": "1", "GVOM_SLOPE_COMPACT": "1"},
-    {"GVOM_COL_EARLY": "1"},
-], ids=["colfast_slopecompact", "col_early"])
+    {"GVOM_COL_EARLY": "1", "GVOM_NEG_DEFER": "0"},
+], ids=["colfast_slopecompact", "col_early_neg_eager"])
 def test_variant_parity(switches):
     env = dict(os.environ, **switches)
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
