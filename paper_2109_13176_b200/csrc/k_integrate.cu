@@ -1160,9 +1160,16 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
   }
   const int64_t threads = tiles * rb.S * rb.tile_threads;
   if (threads == 0) return cudaSuccess;
-  // block size by frame size (see k_raycast): more than two waves of warps
+  // block size by frame size (see k_raycast): more than one wave of warps
   // (SMs x 30 resident warps) -> 128 threads, else 64
-  const bool wide = threads / 32 > 2 * (int64_t)d.sms * 30;
+  // (round 2: above ONE wave -- c3, 1.85 waves, ray cast 68.8 vs 70.4 us with
+  // the 128-thread split kernel; GVOM_RAY_WIDE_WAVES: the threshold, A/B)
+  static int wide_waves = -1;
+  if (wide_waves < 0) {
+    const char* e = getenv("GVOM_RAY_WIDE_WAVES");
+    wide_waves = e ? atoi(e) : 1;
+  }
+  const bool wide = threads / 32 > (int64_t)wide_waves * d.sms * 30;
   const int bs = wide ? 128 : kRayNarrowBS;
   const unsigned blocks = (unsigned)((threads + bs - 1) / bs);
   // schedule by where the REDs land (see aggregate_red_*): the resident one
@@ -1185,8 +1192,8 @@ cudaError_t launch_raycast(const RayBatch& rb, const Dims& d, uint32_t* miss_gri
                                                         *slab);
     return cudaGetLastError();
   }
-  // two warps per 32 rays for frames of more than two waves (c4 -3 %, c5 -4 %;
-  // one- and two-wave frames lose: c2 +7 %); GVOM_RAY_SPLIT=0 / 1 forces it
+  // two warps per 32 rays for the wide frames (c3 -2 %, c4 -3 %, c5 -4 %;
+  // one-wave frames lose: c2 +7 %); GVOM_RAY_SPLIT=0 / 1 forces it
   static int split_env = -2;
   if (split_env == -2) {
     const char* e = getenv("GVOM_RAY_SPLIT");
