@@ -295,3 +295,60 @@ def test_segment_exchange_two_ranks_gloo():
         p.join(timeout=60)
     for rank, status, info, base in res:
         assert status == "ok", info
+
+
+def _worker_gather3(rank, world, port, q):
+    """Three ranks, uneven slab bounds (balanced_slab_rows of a skewed work
+    profile): gather_rows must assemble every rank's rows in place on every
+    rank, for 1-D and 2-D row payloads, and all ranks must agree on the bounds."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import sys
+        sys.path.insert(0, ROOT)
+        from paper_2109_13176_b200 import parallel
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ny = 37
+        work = np.zeros(ny)
+        work[10:20] = 50.0  # skewed: most work in a few rows
+        mine = np.zeros(ny, np.int64)
+        ys0 = [0, 12, 24, ny]  # the frame's (equal-ish) slabs that measured the work
+        mine[ys0[rank]:ys0[rank + 1]] = work[ys0[rank]:ys0[rank + 1]]
+        t = torch.from_numpy(mine)
+        dist.all_reduce(t)
+        yb = parallel.balanced_slab_rows(t.numpy(), world)
+        allyb = [None] * world
+        dist.all_gather_object(allyb, yb)
+        assert all(a == yb for a in allyb)
+        rows = [yb[r + 1] - yb[r] for r in range(world)]
+        assert len(set(rows)) > 1, yb  # uneven
+        for shape in ((ny,), (ny, 5)):
+            full = torch.full(shape, -1, dtype=torch.int32)
+            full[yb[rank]:yb[rank + 1]] = rank * 1000 + torch.arange(yb[rank], yb[rank + 1],
+                                                                    dtype=torch.int32).view(
+                -1, *([1] * (len(shape) - 1)))
+            parallel.gather_rows(full, yb[rank], yb[rank + 1], None, yb)
+            for r in range(world):
+                want = r * 1000 + torch.arange(yb[r], yb[r + 1], dtype=torch.int32)
+                got = full[yb[r]:yb[r + 1]]
+                assert torch.equal(got, want.view(-1, *([1] * (len(shape) - 1))).expand_as(got))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok", yb, None))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "fail", traceback.format_exc(), None))
+
+
+def test_uneven_slab_gather_three_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29200 + (os.getpid() % 200)
+    procs = [ctx.Process(target=_worker_gather3, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info, _ in res:
+        assert status == "ok", info
